@@ -1,0 +1,319 @@
+"""ctypes binding of libspmx_b200.so (include/spmx_b200.h) for tests/ and bench.py.
+
+Python is plumbing here: device memory comes from torch tensors (or the library's own
+allocator), every compute call goes through the C ABI into the hand-written sm_100a
+kernels. There is no CPU fallback: if the shared library is missing this module raises
+at load time, and without a CUDA device every compute call raises SpmxRuntimeError.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+import subprocess
+import sys
+
+import numpy as np
+
+_PKG = os.path.dirname(os.path.abspath(__file__))
+_ROOT = os.path.dirname(_PKG)
+LIB_PATH = os.path.join(_PKG, "libspmx_b200.so")
+CSRC = os.path.join(_PKG, "csrc")
+HEADER = os.path.join(_ROOT, "include", "spmx_b200.h")
+
+ROW, NNZ, MERGE = 0, 1, 2
+STRATEGY = {"row": ROW, "nnz": NNZ, "merge": MERGE}
+EXACT_ORDER = 1
+NO_COOP = 2
+
+NVCC_FLAGS = ["-gencode", "arch=compute_100a,code=sm_100a", "-lineinfo", "-O3", "-std=c++17",
+              "-Xcompiler", "-fPIC", "-shared"]
+
+
+class SpmxInvalidArgument(ValueError):
+    """SPMX_EINVAL — where the reference throws std::invalid_argument."""
+
+
+class SpmxRuntimeError(RuntimeError):
+    """SPMX_ERUNTIME — where the reference throws std::runtime_error."""
+
+
+class SpmxLogicError(RuntimeError):
+    """SPMX_ELOGIC — where the reference throws std::logic_error."""
+
+
+def build_library(force: bool = False, verbose: bool = False) -> str:
+    """Compile csrc/*.cu into libspmx_b200.so for sm_100a (nvcc cross-compiles without a GPU)."""
+    srcs = [os.path.join(CSRC, f) for f in sorted(os.listdir(CSRC)) if f.endswith(".cu")]
+    deps = [os.path.join(CSRC, f) for f in os.listdir(CSRC)] + [HEADER]
+    if not force and os.path.exists(LIB_PATH):
+        if os.path.getmtime(LIB_PATH) >= max(os.path.getmtime(d) for d in deps):
+            return LIB_PATH
+    cmd = ["nvcc", *NVCC_FLAGS, "-o", LIB_PATH, *srcs]
+    if verbose:
+        print(" ".join(cmd), file=sys.stderr)
+    subprocess.check_call(cmd)
+    return LIB_PATH
+
+
+_u64p = C.POINTER(C.c_uint64)
+
+
+def _np_u64(a):
+    return np.ascontiguousarray(a, dtype=np.uint64)
+
+
+class Lib:
+    """Loaded libspmx_b200.so with typed signatures."""
+
+    _inst = None
+
+    @classmethod
+    def get(cls) -> "Lib":
+        if cls._inst is None:
+            cls._inst = cls()
+        return cls._inst
+
+    def __init__(self):
+        if not os.path.exists(LIB_PATH):
+            raise FileNotFoundError(
+                f"{LIB_PATH} is missing: build it with `python -c 'import __graft_entry__ as g; "
+                f"g.build()'` — there is no CPU fallback for this path")
+        L = self.lib = C.CDLL(LIB_PATH)
+        vp, i64, u64, sz = C.c_void_p, C.c_int64, C.c_uint64, C.c_size_t
+        P = C.POINTER
+        L.spmx_last_error.restype = C.c_char_p
+        L.spmx_abi_version.restype = C.c_int
+        L.spmx_kernel_launch_count.restype = u64
+        L.spmx_ctx_create.argtypes = [C.c_int, vp, P(vp)]
+        L.spmx_ctx_destroy.argtypes = [vp]
+        L.spmx_ctx_synchronize.argtypes = [vp]
+        L.spmx_ctx_sm_count.argtypes = [vp, P(C.c_int)]
+        L.spmx_dev_alloc.argtypes = [vp, sz, P(vp)]
+        L.spmx_dev_free.argtypes = [vp, vp]
+        L.spmx_h2d.argtypes = [vp, vp, vp, sz]
+        L.spmx_d2h.argtypes = [vp, vp, vp, sz]
+        L.spmx_host_alloc_pinned.argtypes = [sz, P(vp)]
+        L.spmx_host_free_pinned.argtypes = [vp]
+        L.spmx_csr_upload.argtypes = [vp, i64, i64, i64, vp, vp, vp, P(vp)]
+        L.spmx_csr_wrap_device.argtypes = [vp, i64, i64, i64, vp, vp, vp, C.c_int, P(vp)]
+        L.spmx_csr_destroy.argtypes = [vp]
+        L.spmx_csr_dims.argtypes = [vp, P(i64), P(i64), P(i64)]
+        L.spmx_split_rows_static.argtypes = [vp, u64, C.c_uint, vp]
+        L.spmx_split_nnz.argtypes = [vp, vp, C.c_uint, vp]
+        L.spmx_split_merge.argtypes = [vp, vp, C.c_uint, vp]
+        L.spmx_merge_path_search.argtypes = [vp, vp, sz, vp, vp, vp]
+        L.spmx_next_batch_claims.argtypes = [vp, u64, u64, sz, vp]
+        L.spmx_plan_create.argtypes = [vp, vp, C.c_int, C.c_uint, C.c_int, u64, C.c_uint, P(vp)]
+        L.spmx_plan_destroy.argtypes = [vp]
+        L.spmx_plan_info.argtypes = [vp, P(C.c_uint), P(u64), P(C.c_int)]
+        L.spmx_plan_ranges.argtypes = [vp, vp]
+        L.spmx_plan_chunks.argtypes = [vp, vp, vp]
+        L.spmx_spmm.argtypes = [vp, vp, vp, vp, i64, i64, vp, P(C.c_float)]
+        L.spmx_spmm_host.argtypes = [vp, i64, i64, i64, vp, vp, vp, vp, i64, i64, vp, C.c_int,
+                                     C.c_uint, C.c_int, u64, C.c_uint, P(C.c_double)]
+        L.spmx_checksum_device.argtypes = [vp, vp, sz, P(u64)]
+
+    def check(self, rc: int):
+        if rc == 0:
+            return
+        msg = self.lib.spmx_last_error().decode(errors="replace")
+        raise {1: SpmxInvalidArgument, 2: SpmxRuntimeError, 3: SpmxLogicError}.get(
+            rc, SpmxRuntimeError)(msg)
+
+    def launch_count(self) -> int:
+        return int(self.lib.spmx_kernel_launch_count())
+
+
+def _ptr(a) -> int:
+    """Address of a numpy array / torch tensor / raw int."""
+    if a is None:
+        return 0
+    if isinstance(a, int):
+        return a
+    if isinstance(a, np.ndarray):
+        return a.ctypes.data
+    return a.data_ptr()  # torch tensor
+
+
+class Context:
+    """spmx_ctx: one (device, stream). stream=None creates a private stream; pass a torch
+    stream's .cuda_stream to run on it."""
+
+    def __init__(self, device: int = 0, stream: int | None = None):
+        self.L = Lib.get()
+        h = C.c_void_p()
+        self.L.check(self.L.lib.spmx_ctx_create(device, C.c_void_p(stream or 0), C.byref(h)))
+        self.h = h
+        self.device = device
+
+    def close(self):
+        if self.h:
+            self.L.check(self.L.lib.spmx_ctx_destroy(self.h))
+            self.h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def synchronize(self):
+        self.L.check(self.L.lib.spmx_ctx_synchronize(self.h))
+
+    def sm_count(self) -> int:
+        v = C.c_int()
+        self.L.check(self.L.lib.spmx_ctx_sm_count(self.h, C.byref(v)))
+        return v.value
+
+    # -- CSR ---------------------------------------------------------------------------
+    def csr_upload(self, m, n, row_ptr, col, vals) -> "DeviceCsr":
+        rp = _np_u64(row_ptr)
+        nnz = int(rp[m]) if rp.size > m else -1
+        col = np.ascontiguousarray(col, dtype=np.uint32)
+        vals = np.ascontiguousarray(vals, dtype=np.float32)
+        h = C.c_void_p()
+        self.L.check(self.L.lib.spmx_csr_upload(self.h, m, n, nnz, _ptr(rp), _ptr(col) if col.size else 0,
+                                                _ptr(vals) if vals.size else 0, C.byref(h)))
+        return DeviceCsr(self, h, m, n, nnz)
+
+    def csr_upload_raw(self, m, n, nnz, row_ptr, col, vals) -> "DeviceCsr":
+        """No consistency pre-checks on the host: lets tests feed invalid CSRs."""
+        rp = _np_u64(row_ptr)
+        col = np.ascontiguousarray(col, dtype=np.uint32)
+        vals = np.ascontiguousarray(vals, dtype=np.float32)
+        h = C.c_void_p()
+        self.L.check(self.L.lib.spmx_csr_upload(self.h, m, n, nnz, _ptr(rp), _ptr(col) if col.size else 0,
+                                                _ptr(vals) if vals.size else 0, C.byref(h)))
+        return DeviceCsr(self, h, m, n, nnz)
+
+    def csr_wrap(self, csr, validate=True) -> "DeviceCsr":
+        """Borrow a workloads.Csr whose tensors already live on this device."""
+        h = C.c_void_p()
+        self.L.check(self.L.lib.spmx_csr_wrap_device(self.h, csr.m, csr.n, csr.nnz,
+                                                     _ptr(csr.row_ptr), _ptr(csr.col),
+                                                     _ptr(csr.vals), int(validate), C.byref(h)))
+        d = DeviceCsr(self, h, csr.m, csr.n, csr.nnz)
+        d._keep = csr
+        return d
+
+    # -- partitioner -------------------------------------------------------------------
+    def split_rows_static(self, m, parts):
+        out = np.zeros(2 * max(parts, 1), np.uint64)
+        self.L.check(self.L.lib.spmx_split_rows_static(self.h, m, parts, _ptr(out)))
+        return out.reshape(-1, 2)
+
+    def split_nnz(self, a: "DeviceCsr", parts):
+        out = np.zeros(2 * max(parts, 1), np.uint64)
+        self.L.check(self.L.lib.spmx_split_nnz(self.h, a.h, parts, _ptr(out)))
+        return out.reshape(-1, 2)
+
+    def split_merge(self, a: "DeviceCsr", parts):
+        out = np.zeros(2 * max(parts, 1), np.uint64)
+        self.L.check(self.L.lib.spmx_split_merge(self.h, a.h, parts, _ptr(out)))
+        return out.reshape(-1, 2)
+
+    def merge_path_search(self, a: "DeviceCsr", ks):
+        ks = _np_u64(np.atleast_1d(ks))
+        oi, oj = np.zeros_like(ks), np.zeros_like(ks)
+        self.L.check(self.L.lib.spmx_merge_path_search(self.h, a.h, ks.size, _ptr(ks), _ptr(oi),
+                                                       _ptr(oj)))
+        return oi, oj
+
+    def next_batch_claims(self, m, batch, n_claims):
+        out = np.zeros(2 * max(n_claims, 1), np.uint64)
+        self.L.check(self.L.lib.spmx_next_batch_claims(self.h, m, batch, n_claims, _ptr(out)))
+        return out.reshape(-1, 2)[:n_claims]
+
+    # -- plan / spmm -------------------------------------------------------------------
+    def plan(self, a: "DeviceCsr", strategy="row", parts=0, dynamic=False, batch=128,
+             flags=0) -> "Plan":
+        h = C.c_void_p()
+        s = STRATEGY[strategy] if isinstance(strategy, str) else strategy
+        self.L.check(self.L.lib.spmx_plan_create(self.h, a.h, s, parts, int(dynamic), batch, flags,
+                                                 C.byref(h)))
+        return Plan(self, a, h)
+
+    def spmm(self, plan: "Plan", a: "DeviceCsr", x, y, timed=False):
+        """x: N x d, y: M x d float32 tensors on this device. Returns device ms when timed."""
+        ms = C.c_float(0.0)
+        x_rows, d = x.shape
+        self.L.check(self.L.lib.spmx_spmm(self.h, plan.h, a.h, _ptr(x), x_rows, d, _ptr(y),
+                                          C.byref(ms) if timed else None))
+        return ms.value if timed else None
+
+    def spmm_raw(self, plan, a, x_ptr, x_rows, d, y_ptr):
+        self.L.check(self.L.lib.spmx_spmm(self.h, plan.h, a.h, x_ptr, x_rows, d, y_ptr, None))
+
+    def spmm_host(self, m, n, row_ptr, col, vals, x, y=None, strategy="row", parts=0,
+                  dynamic=False, batch=128, flags=0, nnz=None):
+        """run_spmm with host (numpy) buffers. Returns (y, times_ms dict)."""
+        rp = _np_u64(row_ptr)
+        if nnz is None:
+            nnz = int(rp[m])
+        col = np.ascontiguousarray(col, dtype=np.uint32)
+        vals = np.ascontiguousarray(vals, dtype=np.float32)
+        x = np.ascontiguousarray(x, dtype=np.float32)
+        x_rows, d = x.shape
+        if y is None:
+            y = np.empty((m, d), np.float32)
+        t = (C.c_double * 6)()
+        s = STRATEGY[strategy] if isinstance(strategy, str) else strategy
+        self.L.check(self.L.lib.spmx_spmm_host(self.h, m, n, nnz, _ptr(rp), _ptr(col) if col.size else 0,
+                                               _ptr(vals) if vals.size else 0, _ptr(x), x_rows, d,
+                                               _ptr(y), s, parts, int(dynamic), batch, flags, t))
+        return y, dict(h2d=t[0], plan=t[1], kernel=t[2], d2h=t[3], total=t[4])
+
+    def checksum(self, y) -> int:
+        out = C.c_uint64()
+        self.L.check(self.L.lib.spmx_checksum_device(self.h, _ptr(y), y.numel(), C.byref(out)))
+        return out.value
+
+
+class DeviceCsr:
+    def __init__(self, ctx: Context, h, m, n, nnz):
+        self.ctx, self.h, self.m, self.n, self.nnz = ctx, h, m, n, nnz
+
+    def close(self):
+        if self.h:
+            self.ctx.L.check(self.ctx.L.lib.spmx_csr_destroy(self.h))
+            self.h = None
+
+    def __del__(self):
+        try:
+            if self.ctx.h:
+                self.close()
+        except Exception:
+            pass
+
+
+class Plan:
+    def __init__(self, ctx: Context, a: DeviceCsr, h):
+        self.ctx, self.a, self.h = ctx, a, h
+        p, c, dyn = C.c_uint(), C.c_uint64(), C.c_int()
+        ctx.L.check(ctx.L.lib.spmx_plan_info(h, C.byref(p), C.byref(c), C.byref(dyn)))
+        self.parts, self.n_chunks, self.dynamic = p.value, c.value, bool(dyn.value)
+
+    def ranges(self):
+        if self.dynamic:
+            return np.zeros((0, 2), np.uint64)
+        out = np.zeros(2 * self.parts, np.uint64)
+        self.ctx.L.check(self.ctx.L.lib.spmx_plan_ranges(self.h, _ptr(out)))
+        return out.reshape(-1, 2)
+
+    def chunks(self):
+        r = np.zeros(self.n_chunks + 1, np.uint64)
+        j = np.zeros(self.n_chunks + 1, np.uint64)
+        self.ctx.L.check(self.ctx.L.lib.spmx_plan_chunks(self.h, _ptr(r), _ptr(j)))
+        return r, j
+
+    def close(self):
+        if self.h:
+            self.ctx.L.check(self.ctx.L.lib.spmx_plan_destroy(self.h))
+            self.h = None
+
+    def __del__(self):
+        try:
+            if self.ctx.h:
+                self.close()
+        except Exception:
+            pass

@@ -1,0 +1,832 @@
+// spmx_capi.cu — implementation of include/spmx_b200.h (the C ABI of the B200 SpMM path).
+//
+// Host-side orchestration only: handle lifetime, argument checks with the reference's
+// error behaviour, plan construction (partition.cuh kernels) and kernel dispatch per d
+// (the GPU counterpart of the reference's per-d code generation, src/plan.cpp:42-93 and
+// src/jit.cpp:136-154: everything that depends on d is fixed before the hot loop).
+#include "../../include/spmx_b200.h"
+
+#include <cuda_runtime.h>
+
+#include <atomic>
+#include <cstdio>
+#include <cstring>
+#include <exception>
+#include <new>
+#include <stdexcept>
+#include <string>
+#include <vector>
+
+#include "spmx_kernels.cuh"
+#include "spmx_partition.cuh"
+
+using spmx_dev::u64;
+
+namespace {
+
+thread_local std::string g_last_error;
+std::atomic<uint64_t> g_launches{0};
+
+struct InvalidArg : std::runtime_error { using std::runtime_error::runtime_error; };
+struct LogicErr : std::runtime_error { using std::runtime_error::runtime_error; };
+
+#define CUDA_CHECK(expr)                                                                   \
+  do {                                                                                     \
+    cudaError_t _e = (expr);                                                               \
+    if (_e != cudaSuccess)                                                                 \
+      throw std::runtime_error(std::string("CUDA error: ") + cudaGetErrorString(_e) +      \
+                               " at " #expr);                                              \
+  } while (0)
+
+template <typename F>
+int guarded(F&& f) {
+  try {
+    f();
+    return SPMX_OK;
+  } catch (const InvalidArg& e) {
+    g_last_error = e.what();
+    return SPMX_EINVAL;
+  } catch (const LogicErr& e) {
+    g_last_error = e.what();
+    return SPMX_ELOGIC;
+  } catch (const std::bad_alloc&) {
+    g_last_error = "out of host memory";
+    return SPMX_ERUNTIME;
+  } catch (const std::exception& e) {
+    g_last_error = e.what();
+    return SPMX_ERUNTIME;
+  }
+}
+
+constexpr uint32_t kMagicCtx = 0x58435443, kMagicCsr = 0x58435352, kMagicPlan = 0x58504c4e;
+constexpr u64 kDefaultChunkItems = 1024;  // merge items (rows + nonzeros) per warp-level chunk
+constexpr unsigned kDefaultLongSeg = 64;  // row segments >= this are shared by the warp's groups
+
+inline unsigned blocks_for(u64 n, unsigned threads = 256) {
+  return (unsigned)((n + threads - 1) / threads);
+}
+
+}  // namespace
+
+struct spmx_ctx {
+  uint32_t magic = kMagicCtx;
+  int device = 0;
+  cudaStream_t stream = nullptr;
+  bool own_stream = false;
+  int sm_count = 0;
+  cudaEvent_t ev0 = nullptr, ev1 = nullptr;
+  int* d_err = nullptr;  // device-side error flag for validation
+  // grow-only staging used by spmx_spmm_host
+  void* ws[5] = {nullptr, nullptr, nullptr, nullptr, nullptr};
+  size_t ws_bytes[5] = {0, 0, 0, 0, 0};
+};
+
+struct spmx_csr {
+  uint32_t magic = kMagicCsr;
+  spmx_ctx* ctx = nullptr;
+  int64_t m = 0, n = 0, nnz = 0;
+  u64* row_ptr = nullptr;
+  uint32_t* col = nullptr;
+  float* vals = nullptr;
+  bool owned = false;
+};
+
+struct spmx_plan {
+  uint32_t magic = kMagicPlan;
+  spmx_ctx* ctx = nullptr;
+  const spmx_csr* csr = nullptr;
+  int strategy = 0;
+  unsigned parts = 0;
+  unsigned flags = 0;
+  bool dynamic = false;
+  u64 batch = 128;
+  u64 n_chunks = 0;
+  u64* ranges = nullptr;     // 2*parts, device (absent under dynamic dispatch)
+  u64* chunk_row = nullptr;  // n_chunks+1
+  u64* chunk_nnz = nullptr;  // n_chunks+1
+  u64* counter = nullptr;    // dynamic dispatch
+  bool may_carry = false;
+  mutable float* carry = nullptr;  // n_chunks x ld floats, grown on demand
+  mutable size_t carry_floats = 0;
+};
+
+namespace {
+
+spmx_ctx* check(spmx_ctx* c) {
+  if (!c || c->magic != kMagicCtx) throw LogicErr("invalid or destroyed spmx_ctx");
+  CUDA_CHECK(cudaSetDevice(c->device));
+  return c;
+}
+const spmx_csr* check(const spmx_csr* a) {
+  if (!a || a->magic != kMagicCsr) throw LogicErr("invalid or destroyed spmx_csr");
+  return a;
+}
+const spmx_plan* check(const spmx_plan* p) {
+  if (!p || p->magic != kMagicPlan) throw LogicErr("invalid or destroyed spmx_plan");
+  return p;
+}
+
+template <typename T>
+T* dev_alloc(size_t count) {
+  T* p = nullptr;
+  CUDA_CHECK(cudaMalloc(&p, (count ? count : 1) * sizeof(T)));
+  return p;
+}
+
+void launched(unsigned n = 1) { g_launches.fetch_add(n, std::memory_order_relaxed); }
+
+void post_launch() {
+  launched();
+  CUDA_CHECK(cudaGetLastError());
+}
+
+// ---- partition boundaries on the device --------------------------------------------------
+// Fills bnd[0..parts] (row boundaries) for the strategy, row-snapped.
+void strategy_row_boundaries(spmx_ctx* ctx, const spmx_csr* a, int strategy, unsigned parts,
+                             u64* d_bnd) {
+  const unsigned nb = blocks_for((u64)parts + 1);
+  switch (strategy) {
+    case SPMX_ROW_SPLIT:
+      spmx_dev::row_boundaries_kernel<<<nb, 256, 0, ctx->stream>>>((u64)a->m, parts, d_bnd);
+      break;
+    case SPMX_NNZ_SPLIT:
+      spmx_dev::nnz_boundaries_kernel<<<nb, 256, 0, ctx->stream>>>(a->row_ptr, (u64)a->m,
+                                                                   (u64)a->nnz, parts, d_bnd);
+      break;
+    case SPMX_MERGE_SPLIT:
+      spmx_dev::merge_boundaries_kernel<<<nb, 256, 0, ctx->stream>>>(
+          a->row_ptr, (u64)a->m, (u64)a->nnz, parts, 1, d_bnd);
+      break;
+    default:
+      throw InvalidArg("unknown strategy");
+  }
+  post_launch();
+}
+
+void ranges_to_host(spmx_ctx* ctx, const u64* d_bnd, unsigned parts, uint64_t* out) {
+  u64* d_ranges = dev_alloc<u64>(2 * (size_t)parts);
+  spmx_dev::ranges_from_boundaries_kernel<<<blocks_for(parts), 256, 0, ctx->stream>>>(
+      d_bnd, parts, d_ranges);
+  post_launch();
+  CUDA_CHECK(cudaMemcpyAsync(out, d_ranges, 2 * (size_t)parts * sizeof(u64),
+                             cudaMemcpyDeviceToHost, ctx->stream));
+  CUDA_CHECK(cudaStreamSynchronize(ctx->stream));
+  CUDA_CHECK(cudaFree(d_ranges));
+}
+
+void validate_on_device(spmx_ctx* ctx, const spmx_csr* a) {
+  CUDA_CHECK(cudaMemsetAsync(ctx->d_err, 0, sizeof(int), ctx->stream));
+  const unsigned nb = (unsigned)std::min<u64>(
+      (u64)ctx->sm_count * 8, std::max<u64>(1, ((u64)a->nnz + (u64)a->m + 255) / 256));
+  spmx_dev::validate_csr_kernel<<<nb, 256, 0, ctx->stream>>>(a->row_ptr, a->col, (u64)a->m,
+                                                             (u64)a->n, (u64)a->nnz, ctx->d_err);
+  post_launch();
+  int err = 0;
+  CUDA_CHECK(cudaMemcpyAsync(&err, ctx->d_err, sizeof(int), cudaMemcpyDeviceToHost, ctx->stream));
+  CUDA_CHECK(cudaStreamSynchronize(ctx->stream));
+  static const char* what[] = {"", "", "row_ptr[0] != 0", "row_ptr[m] != nnz",
+                               "row_ptr not nondecreasing", "column index out of range"};
+  if (err) throw InvalidArg(std::string("invalid CSR: ") + what[err]);
+}
+
+// ---- kernel dispatch per d ------------------------------------------------------------------
+struct Shape {
+  int d_ct, g, vec, nt;
+};
+
+template <int D_CT, int G, int VEC, int NT, bool RAGGED>
+void launch_one(const spmx_plan* p, const spmx_dev::SpmmArgs& args, cudaStream_t st, int sm_count) {
+  if (p->dynamic) {
+    int occ = 0;
+    CUDA_CHECK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(
+        &occ, spmx_dev::spmm_dynamic_kernel<D_CT, G, VEC, NT, RAGGED>, spmx_dev::kWarpsPerCta * 32,
+        0));
+    const unsigned grid = (unsigned)(sm_count * (occ > 0 ? occ : 1));
+    spmx_dev::spmm_dynamic_kernel<D_CT, G, VEC, NT, RAGGED>
+        <<<grid, spmx_dev::kWarpsPerCta * 32, 0, st>>>(args);
+  } else {
+    const unsigned grid =
+        (unsigned)((args.n_chunks + spmx_dev::kWarpsPerCta - 1) / spmx_dev::kWarpsPerCta);
+    if (grid == 0) return;
+    spmx_dev::spmm_chunk_kernel<D_CT, G, VEC, NT, RAGGED>
+        <<<grid, spmx_dev::kWarpsPerCta * 32, 0, st>>>(args);
+  }
+  post_launch();
+}
+
+template <int VEC>
+void launch_generic(const spmx_plan* p, const spmx_dev::SpmmArgs& a, int g, int nt,
+                    cudaStream_t st, int sms) {
+  if (nt == 1) {
+    switch (g) {
+      case 1: return launch_one<0, 1, VEC, 1, true>(p, a, st, sms);
+      case 2: return launch_one<0, 2, VEC, 1, true>(p, a, st, sms);
+      case 4: return launch_one<0, 4, VEC, 1, true>(p, a, st, sms);
+      case 8: return launch_one<0, 8, VEC, 1, true>(p, a, st, sms);
+      case 16: return launch_one<0, 16, VEC, 1, true>(p, a, st, sms);
+      case 32: return launch_one<0, 32, VEC, 1, true>(p, a, st, sms);
+    }
+  } else if (g == 32) {
+    switch (nt) {
+      case 2: return launch_one<0, 32, VEC, 2, true>(p, a, st, sms);
+      case 4: return launch_one<0, 32, VEC, 4, true>(p, a, st, sms);
+      case 8: return launch_one<0, 32, VEC, 8, true>(p, a, st, sms);
+    }
+  }
+  throw std::runtime_error("internal: no kernel for this shape");
+}
+
+int pow2_ceil(int v) {
+  int p = 1;
+  while (p < v) p <<= 1;
+  return p;
+}
+
+void run_kernels(spmx_ctx* ctx, const spmx_plan* p, const spmx_csr* a, const float* d_x,
+                 int64_t d, float* d_y) {
+  if (a->m == 0) return;
+  const bool aligned16 = ((uintptr_t)d_x % 16 == 0) && ((uintptr_t)d_y % 16 == 0);
+  const int vec = (d % 4 == 0 && aligned16) ? 4 : 1;
+  const int slab_max = 32 * vec * 8;  // G=32, NT=8
+
+  if (p->may_carry) {
+    const size_t need = (size_t)p->n_chunks * (size_t)d;
+    if (need > p->carry_floats) {
+      if (p->carry) CUDA_CHECK(cudaFree(p->carry));
+      p->carry = dev_alloc<float>(need);
+      p->carry_floats = need;
+    }
+  }
+
+  spmx_dev::SpmmArgs args{};
+  args.row_ptr = a->row_ptr;
+  args.col = a->col;
+  args.vals = a->vals;
+  args.x = d_x;
+  args.y = d_y;
+  args.carry_out = p->may_carry ? p->carry : nullptr;
+  args.chunk_row = p->chunk_row;
+  args.chunk_nnz = p->chunk_nnz;
+  args.n_chunks = p->n_chunks;
+  args.m = (u64)a->m;
+  args.ldx = (int)d;
+  const bool exact = (p->flags & SPMX_EXACT_ORDER) != 0;
+  args.long_seg = (exact || (p->flags & SPMX_NO_COOP)) ? 0u : kDefaultLongSeg;
+  args.counter = p->counter;
+  args.batch = p->batch;
+
+  for (int64_t c0 = 0; c0 < d; c0 += slab_max) {
+    const int dw = (int)std::min<int64_t>(slab_max, d - c0);
+    args.c0 = (int)c0;
+    args.dw = dw;
+    if (p->dynamic) CUDA_CHECK(cudaMemsetAsync(p->counter, 0, sizeof(u64), ctx->stream));
+    if (vec == 4 && c0 == 0 && d == 32) {
+      launch_one<32, 8, 4, 1, false>(p, args, ctx->stream, ctx->sm_count);
+    } else if (vec == 4 && c0 == 0 && d == 64) {
+      launch_one<64, 16, 4, 1, false>(p, args, ctx->stream, ctx->sm_count);
+    } else if (vec == 4 && c0 == 0 && d == 128) {
+      launch_one<128, 32, 4, 1, false>(p, args, ctx->stream, ctx->sm_count);
+    } else {
+      const int lanes = (dw + vec - 1) / vec;
+      int g = pow2_ceil(std::min(lanes, 32));
+      int nt = 1;
+      if (lanes > 32) nt = pow2_ceil((lanes + 31) / 32);
+      if (vec == 4)
+        launch_generic<4>(p, args, g, nt, ctx->stream, ctx->sm_count);
+      else
+        launch_generic<1>(p, args, g, nt, ctx->stream, ctx->sm_count);
+    }
+    if (p->may_carry && p->n_chunks > 1) {
+      spmx_dev::carry_fixup_kernel<<<(unsigned)(p->n_chunks - 1), 128, 0, ctx->stream>>>(
+          a->row_ptr, p->chunk_row, p->chunk_nnz, p->n_chunks, (u64)a->m, p->carry, d_y, (int)d,
+          (int)c0, dw);
+      post_launch();
+    }
+  }
+}
+
+void plan_free(spmx_plan* p) {
+  if (!p) return;
+  if (p->ranges) cudaFree(p->ranges);
+  if (p->chunk_row) cudaFree(p->chunk_row);
+  if (p->chunk_nnz) cudaFree(p->chunk_nnz);
+  if (p->counter) cudaFree(p->counter);
+  if (p->carry) cudaFree(p->carry);
+  p->magic = 0;
+  delete p;
+}
+
+spmx_plan* plan_build(spmx_ctx* ctx, const spmx_csr* a, int strategy, unsigned parts, int dynamic,
+                      uint64_t batch, unsigned flags) {
+  if (strategy < 0 || strategy > 2) throw InvalidArg("make_partition: unknown strategy");
+  if (dynamic) {
+    // partition.cpp:91-94
+    if (strategy != SPMX_ROW_SPLIT)
+      throw InvalidArg("dynamic dispatch pairs with row-split only");
+    if (batch == 0) throw InvalidArg("batch_size must be >= 1");
+  }
+  const u64 m = (u64)a->m, nnz = (u64)a->nnz;
+  const bool exact = (flags & SPMX_EXACT_ORDER) != 0;
+  if (parts == 0) {
+    const u64 want = (m + nnz + kDefaultChunkItems - 1) / kDefaultChunkItems;
+    parts = (unsigned)std::min<u64>(std::max<u64>(want, 1), 1u << 30);
+  }
+  spmx_plan* p = new spmx_plan;
+  try {
+    p->ctx = ctx;
+    p->csr = a;
+    p->strategy = strategy;
+    p->parts = parts;
+    p->flags = flags;
+    p->dynamic = dynamic != 0;
+    p->batch = batch ? batch : 128;
+    if (p->dynamic) {
+      p->counter = dev_alloc<u64>(1);
+      CUDA_CHECK(cudaMemsetAsync(p->counter, 0, sizeof(u64), ctx->stream));
+      return p;
+    }
+    // 1. the strategy's row-snapped boundaries and RowRange list (bit-exact with the reference)
+    u64* d_bnd = dev_alloc<u64>((size_t)parts + 1);
+    strategy_row_boundaries(ctx, a, strategy, parts, d_bnd);
+    p->ranges = dev_alloc<u64>(2 * (size_t)parts);
+    spmx_dev::ranges_from_boundaries_kernel<<<blocks_for(parts), 256, 0, ctx->stream>>>(
+        d_bnd, parts, p->ranges);
+    post_launch();
+    // 2. strategy-level merge-path diagonals
+    u64* d_diag = dev_alloc<u64>((size_t)parts + 1);
+    if (strategy == SPMX_MERGE_SPLIT && !exact) {
+      spmx_dev::merge_boundaries_kernel<<<blocks_for((u64)parts + 1), 256, 0, ctx->stream>>>(
+          a->row_ptr, m, nnz, parts, 0, d_diag);
+    } else {
+      spmx_dev::boundaries_to_diagonals_kernel<<<blocks_for((u64)parts + 1), 256, 0, ctx->stream>>>(
+          a->row_ptr, d_bnd, (u64)parts + 1, d_diag);
+    }
+    post_launch();
+    // 3. work list: exact -> one chunk per range; otherwise ranges heavier than the chunk budget
+    //    are cut along the merge path
+    u64* d_cdiag = nullptr;
+    if (exact) {
+      p->n_chunks = parts;
+      d_cdiag = d_diag;
+      d_diag = nullptr;
+    } else {
+      u64* d_cnt = dev_alloc<u64>(parts);
+      u64* d_off = dev_alloc<u64>((size_t)parts + 1);
+      spmx_dev::count_chunks_kernel<<<blocks_for(parts), 256, 0, ctx->stream>>>(
+          d_diag, parts, kDefaultChunkItems, d_cnt);
+      post_launch();
+      spmx_dev::exclusive_scan_kernel<<<1, 1024, 0, ctx->stream>>>(d_cnt, parts, d_off);
+      post_launch();
+      u64 total = 0;
+      CUDA_CHECK(cudaMemcpyAsync(&total, d_off + parts, sizeof(u64), cudaMemcpyDeviceToHost,
+                                 ctx->stream));
+      CUDA_CHECK(cudaStreamSynchronize(ctx->stream));
+      p->n_chunks = total;
+      d_cdiag = dev_alloc<u64>((size_t)total + 1);
+      spmx_dev::chunk_diagonals_kernel<<<blocks_for(total + 1), 256, 0, ctx->stream>>>(
+          d_diag, d_off, parts, total, d_cdiag);
+      post_launch();
+      CUDA_CHECK(cudaStreamSynchronize(ctx->stream));
+      CUDA_CHECK(cudaFree(d_cnt));
+      CUDA_CHECK(cudaFree(d_off));
+      p->may_carry = true;
+    }
+    p->chunk_row = dev_alloc<u64>((size_t)p->n_chunks + 1);
+    p->chunk_nnz = dev_alloc<u64>((size_t)p->n_chunks + 1);
+    spmx_dev::merge_search_kernel<<<blocks_for(p->n_chunks + 1), 256, 0, ctx->stream>>>(
+        a->row_ptr, m, nnz, d_cdiag, p->n_chunks + 1, p->chunk_row, p->chunk_nnz);
+    post_launch();
+    CUDA_CHECK(cudaStreamSynchronize(ctx->stream));
+    CUDA_CHECK(cudaFree(d_cdiag));
+    if (d_diag) CUDA_CHECK(cudaFree(d_diag));
+    CUDA_CHECK(cudaFree(d_bnd));
+    return p;
+  } catch (...) {
+    plan_free(p);
+    throw;
+  }
+}
+
+void* ws_get(spmx_ctx* ctx, int slot, size_t bytes) {
+  if (ctx->ws_bytes[slot] < bytes) {
+    if (ctx->ws[slot]) CUDA_CHECK(cudaFree(ctx->ws[slot]));
+    ctx->ws[slot] = nullptr;
+    ctx->ws_bytes[slot] = 0;
+    CUDA_CHECK(cudaMalloc(&ctx->ws[slot], bytes ? bytes : 1));
+    ctx->ws_bytes[slot] = bytes;
+  }
+  return ctx->ws[slot];
+}
+
+}  // namespace
+
+extern "C" {
+
+const char* spmx_last_error(void) { return g_last_error.c_str(); }
+int spmx_abi_version(void) { return 1; }
+uint64_t spmx_kernel_launch_count(void) { return g_launches.load(); }
+
+int spmx_ctx_create(int device, void* stream, spmx_ctx** out) {
+  return guarded([&] {
+    if (!out) throw InvalidArg("spmx_ctx_create: null out");
+    int count = 0;
+    cudaError_t e = cudaGetDeviceCount(&count);
+    if (e != cudaSuccess || count == 0)
+      throw std::runtime_error(
+          "no CUDA device: this library has no CPU fallback (cudaGetDeviceCount: " +
+          std::string(cudaGetErrorString(e)) + ")");
+    if (device < 0 || device >= count) throw InvalidArg("spmx_ctx_create: no such device");
+    CUDA_CHECK(cudaSetDevice(device));
+    spmx_ctx* c = new spmx_ctx;
+    c->device = device;
+    if (stream) {
+      c->stream = (cudaStream_t)stream;
+    } else {
+      CUDA_CHECK(cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking));
+      c->own_stream = true;
+    }
+    CUDA_CHECK(cudaDeviceGetAttribute(&c->sm_count, cudaDevAttrMultiProcessorCount, device));
+    CUDA_CHECK(cudaEventCreate(&c->ev0));
+    CUDA_CHECK(cudaEventCreate(&c->ev1));
+    c->d_err = dev_alloc<int>(1);
+    *out = c;
+  });
+}
+
+int spmx_ctx_destroy(spmx_ctx* ctx) {
+  return guarded([&] {
+    check(ctx);
+    cudaStreamSynchronize(ctx->stream);
+    for (int i = 0; i < 5; ++i)
+      if (ctx->ws[i]) cudaFree(ctx->ws[i]);
+    cudaFree(ctx->d_err);
+    cudaEventDestroy(ctx->ev0);
+    cudaEventDestroy(ctx->ev1);
+    if (ctx->own_stream) cudaStreamDestroy(ctx->stream);
+    ctx->magic = 0;
+    delete ctx;
+  });
+}
+
+int spmx_ctx_synchronize(spmx_ctx* ctx) {
+  return guarded([&] { CUDA_CHECK(cudaStreamSynchronize(check(ctx)->stream)); });
+}
+
+int spmx_ctx_sm_count(spmx_ctx* ctx, int* out) {
+  return guarded([&] { *out = check(ctx)->sm_count; });
+}
+
+int spmx_dev_alloc(spmx_ctx* ctx, size_t bytes, void** out) {
+  return guarded([&] {
+    check(ctx);
+    CUDA_CHECK(cudaMalloc(out, bytes ? bytes : 1));
+  });
+}
+int spmx_dev_free(spmx_ctx* ctx, void* ptr) {
+  return guarded([&] {
+    check(ctx);
+    CUDA_CHECK(cudaFree(ptr));
+  });
+}
+int spmx_h2d(spmx_ctx* ctx, void* dst, const void* src, size_t bytes) {
+  return guarded([&] {
+    CUDA_CHECK(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyHostToDevice, check(ctx)->stream));
+  });
+}
+int spmx_d2h(spmx_ctx* ctx, void* dst, const void* src, size_t bytes) {
+  return guarded([&] {
+    CUDA_CHECK(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyDeviceToHost, check(ctx)->stream));
+  });
+}
+int spmx_host_alloc_pinned(size_t bytes, void** out) {
+  return guarded([&] { CUDA_CHECK(cudaMallocHost(out, bytes ? bytes : 1)); });
+}
+int spmx_host_free_pinned(void* ptr) {
+  return guarded([&] { CUDA_CHECK(cudaFreeHost(ptr)); });
+}
+
+int spmx_csr_upload(spmx_ctx* ctx, int64_t m, int64_t n, int64_t nnz, const uint64_t* row_ptr,
+                    const uint32_t* col, const float* vals, spmx_csr** out) {
+  return guarded([&] {
+    check(ctx);
+    if (!out) throw InvalidArg("spmx_csr_upload: null out");
+    if (m < 0 || n < 0 || nnz < 0) throw InvalidArg("invalid CSR: negative dimension");
+    if (!row_ptr || (nnz > 0 && (!col || !vals))) throw InvalidArg("invalid CSR: null array");
+    spmx_csr* a = new spmx_csr;
+    a->ctx = ctx;
+    a->m = m;
+    a->n = n;
+    a->nnz = nnz;
+    a->owned = true;
+    try {
+      a->row_ptr = dev_alloc<u64>((size_t)m + 1);
+      a->col = dev_alloc<uint32_t>((size_t)nnz);
+      a->vals = dev_alloc<float>((size_t)nnz);
+      CUDA_CHECK(cudaMemcpyAsync(a->row_ptr, row_ptr, ((size_t)m + 1) * 8, cudaMemcpyHostToDevice,
+                                 ctx->stream));
+      if (nnz) {
+        CUDA_CHECK(cudaMemcpyAsync(a->col, col, (size_t)nnz * 4, cudaMemcpyHostToDevice,
+                                   ctx->stream));
+        CUDA_CHECK(cudaMemcpyAsync(a->vals, vals, (size_t)nnz * 4, cudaMemcpyHostToDevice,
+                                   ctx->stream));
+      }
+      validate_on_device(ctx, a);
+    } catch (...) {
+      spmx_csr_destroy(a);
+      throw;
+    }
+    *out = a;
+  });
+}
+
+int spmx_csr_wrap_device(spmx_ctx* ctx, int64_t m, int64_t n, int64_t nnz, const uint64_t* d_rp,
+                         const uint32_t* d_col, const float* d_vals, int validate,
+                         spmx_csr** out) {
+  return guarded([&] {
+    check(ctx);
+    if (!out) throw InvalidArg("spmx_csr_wrap_device: null out");
+    if (m < 0 || n < 0 || nnz < 0) throw InvalidArg("invalid CSR: negative dimension");
+    if (!d_rp) throw InvalidArg("invalid CSR: null row_ptr");
+    spmx_csr* a = new spmx_csr;
+    a->ctx = ctx;
+    a->m = m;
+    a->n = n;
+    a->nnz = nnz;
+    a->row_ptr = (u64*)d_rp;
+    a->col = (uint32_t*)d_col;
+    a->vals = (float*)d_vals;
+    a->owned = false;
+    try {
+      if (validate) validate_on_device(ctx, a);
+    } catch (...) {
+      spmx_csr_destroy(a);
+      throw;
+    }
+    *out = a;
+  });
+}
+
+int spmx_csr_destroy(spmx_csr* a) {
+  return guarded([&] {
+    check((const spmx_csr*)a);
+    if (a->owned) {
+      cudaFree(a->row_ptr);
+      cudaFree(a->col);
+      cudaFree(a->vals);
+    }
+    a->magic = 0;
+    delete a;
+  });
+}
+
+int spmx_csr_dims(const spmx_csr* a, int64_t* m, int64_t* n, int64_t* nnz) {
+  return guarded([&] {
+    check(a);
+    if (m) *m = a->m;
+    if (n) *n = a->n;
+    if (nnz) *nnz = a->nnz;
+  });
+}
+
+int spmx_split_rows_static(spmx_ctx* ctx, uint64_t m, unsigned parts, uint64_t* out) {
+  return guarded([&] {
+    check(ctx);
+    if (parts == 0) throw InvalidArg("split_rows_static: zero threads");
+    u64* d_bnd = dev_alloc<u64>((size_t)parts + 1);
+    spmx_dev::row_boundaries_kernel<<<blocks_for((u64)parts + 1), 256, 0, ctx->stream>>>(
+        (u64)m, parts, d_bnd);
+    post_launch();
+    ranges_to_host(ctx, d_bnd, parts, out);
+    CUDA_CHECK(cudaFree(d_bnd));
+  });
+}
+
+int spmx_split_nnz(spmx_ctx* ctx, const spmx_csr* a, unsigned parts, uint64_t* out) {
+  return guarded([&] {
+    check(ctx);
+    check(a);
+    if (parts == 0) throw InvalidArg("split_nnz: zero threads");
+    u64* d_bnd = dev_alloc<u64>((size_t)parts + 1);
+    strategy_row_boundaries(ctx, a, SPMX_NNZ_SPLIT, parts, d_bnd);
+    ranges_to_host(ctx, d_bnd, parts, out);
+    CUDA_CHECK(cudaFree(d_bnd));
+  });
+}
+
+int spmx_split_merge(spmx_ctx* ctx, const spmx_csr* a, unsigned parts, uint64_t* out) {
+  return guarded([&] {
+    check(ctx);
+    check(a);
+    if (parts == 0) throw InvalidArg("split_merge: zero threads");
+    u64* d_bnd = dev_alloc<u64>((size_t)parts + 1);
+    strategy_row_boundaries(ctx, a, SPMX_MERGE_SPLIT, parts, d_bnd);
+    ranges_to_host(ctx, d_bnd, parts, out);
+    CUDA_CHECK(cudaFree(d_bnd));
+  });
+}
+
+int spmx_merge_path_search(spmx_ctx* ctx, const spmx_csr* a, size_t n_diag, const uint64_t* k,
+                           uint64_t* out_i, uint64_t* out_j) {
+  return guarded([&] {
+    check(ctx);
+    check(a);
+    const u64 lim = (u64)a->m + (u64)a->nnz;
+    for (size_t t = 0; t < n_diag; ++t)
+      if (k[t] > lim) throw InvalidArg("merge_path_search: diagonal out of range");
+    if (n_diag == 0) return;
+    u64* d_k = dev_alloc<u64>(n_diag);
+    u64* d_i = dev_alloc<u64>(n_diag);
+    u64* d_j = dev_alloc<u64>(n_diag);
+    CUDA_CHECK(cudaMemcpyAsync(d_k, k, n_diag * 8, cudaMemcpyHostToDevice, ctx->stream));
+    spmx_dev::merge_search_kernel<<<blocks_for(n_diag), 256, 0, ctx->stream>>>(
+        a->row_ptr, (u64)a->m, (u64)a->nnz, d_k, n_diag, d_i, d_j);
+    post_launch();
+    CUDA_CHECK(cudaMemcpyAsync(out_i, d_i, n_diag * 8, cudaMemcpyDeviceToHost, ctx->stream));
+    CUDA_CHECK(cudaMemcpyAsync(out_j, d_j, n_diag * 8, cudaMemcpyDeviceToHost, ctx->stream));
+    CUDA_CHECK(cudaStreamSynchronize(ctx->stream));
+    CUDA_CHECK(cudaFree(d_k));
+    CUDA_CHECK(cudaFree(d_i));
+    CUDA_CHECK(cudaFree(d_j));
+  });
+}
+
+int spmx_next_batch_claims(spmx_ctx* ctx, uint64_t m, uint64_t batch, size_t n_claims,
+                           uint64_t* out) {
+  return guarded([&] {
+    check(ctx);
+    if (batch == 0) throw InvalidArg("batch_size must be >= 1");
+    if (n_claims == 0) return;
+    u64* d_counter = dev_alloc<u64>(1);
+    u64* d_out = dev_alloc<u64>(2 * n_claims);
+    CUDA_CHECK(cudaMemsetAsync(d_counter, 0, 8, ctx->stream));
+    spmx_dev::next_batch_claims_kernel<<<blocks_for(n_claims), 256, 0, ctx->stream>>>(
+        d_counter, (u64)batch, (u64)m, (u64)n_claims, d_out);
+    post_launch();
+    CUDA_CHECK(cudaMemcpyAsync(out, d_out, 2 * n_claims * 8, cudaMemcpyDeviceToHost, ctx->stream));
+    CUDA_CHECK(cudaStreamSynchronize(ctx->stream));
+    CUDA_CHECK(cudaFree(d_counter));
+    CUDA_CHECK(cudaFree(d_out));
+  });
+}
+
+int spmx_plan_create(spmx_ctx* ctx, const spmx_csr* a, int strategy, unsigned parts, int dynamic,
+                     uint64_t batch, unsigned flags, spmx_plan** out) {
+  return guarded([&] {
+    check(ctx);
+    check(a);
+    if (!out) throw InvalidArg("spmx_plan_create: null out");
+    if (a->ctx != ctx) throw LogicErr("spmx_plan_create: csr belongs to another context");
+    *out = plan_build(ctx, a, strategy, parts, dynamic, batch, flags);
+  });
+}
+
+int spmx_plan_destroy(spmx_plan* p) {
+  return guarded([&] {
+    check((const spmx_plan*)p);
+    CUDA_CHECK(cudaSetDevice(p->ctx->device));
+    plan_free(p);
+  });
+}
+
+int spmx_plan_info(const spmx_plan* p, unsigned* parts, uint64_t* n_chunks, int* dynamic) {
+  return guarded([&] {
+    check(p);
+    if (parts) *parts = p->parts;
+    if (n_chunks) *n_chunks = p->n_chunks;
+    if (dynamic) *dynamic = p->dynamic ? 1 : 0;
+  });
+}
+
+int spmx_plan_ranges(const spmx_plan* p, uint64_t* out) {
+  return guarded([&] {
+    check(p);
+    check(p->ctx);
+    if (p->dynamic) return;  // WorkPartition.ranges is empty under dynamic dispatch
+    CUDA_CHECK(cudaMemcpyAsync(out, p->ranges, 2 * (size_t)p->parts * 8, cudaMemcpyDeviceToHost,
+                               p->ctx->stream));
+    CUDA_CHECK(cudaStreamSynchronize(p->ctx->stream));
+  });
+}
+
+int spmx_plan_chunks(const spmx_plan* p, uint64_t* out_row, uint64_t* out_nnz) {
+  return guarded([&] {
+    check(p);
+    check(p->ctx);
+    if (p->dynamic) return;
+    const size_t bytes = ((size_t)p->n_chunks + 1) * 8;
+    CUDA_CHECK(cudaMemcpyAsync(out_row, p->chunk_row, bytes, cudaMemcpyDeviceToHost, p->ctx->stream));
+    CUDA_CHECK(cudaMemcpyAsync(out_nnz, p->chunk_nnz, bytes, cudaMemcpyDeviceToHost, p->ctx->stream));
+    CUDA_CHECK(cudaStreamSynchronize(p->ctx->stream));
+  });
+}
+
+int spmx_spmm(spmx_ctx* ctx, const spmx_plan* plan, const spmx_csr* a, const float* d_x,
+              int64_t x_rows, int64_t d, float* d_y, float* elapsed_ms) {
+  return guarded([&] {
+    check(ctx);
+    check(plan);
+    check(a);
+    if (plan->csr != a || plan->ctx != ctx)
+      throw LogicErr("spmx_spmm: plan was built for another matrix or context");
+    if (a->n != x_rows) throw InvalidArg("run_spmm: A.n != X.rows");  // executor.cpp:38
+    if (d < 1) throw InvalidArg("run_spmm: X.cols must be >= 1");
+    if (d > (1 << 30)) throw InvalidArg("run_spmm: X.cols too large");
+    if ((!d_x && a->n > 0) || (!d_y && a->m > 0)) throw InvalidArg("run_spmm: null X or Y");
+    if (elapsed_ms) CUDA_CHECK(cudaEventRecord(ctx->ev0, ctx->stream));
+    run_kernels(ctx, plan, a, d_x, d, d_y);
+    if (elapsed_ms) {
+      CUDA_CHECK(cudaEventRecord(ctx->ev1, ctx->stream));
+      CUDA_CHECK(cudaEventSynchronize(ctx->ev1));
+      CUDA_CHECK(cudaEventElapsedTime(elapsed_ms, ctx->ev0, ctx->ev1));
+    }
+  });
+}
+
+int spmx_spmm_host(spmx_ctx* ctx, int64_t m, int64_t n, int64_t nnz, const uint64_t* row_ptr,
+                   const uint32_t* col, const float* vals, const float* x, int64_t x_rows,
+                   int64_t d, float* y, int strategy, unsigned parts, int dynamic, uint64_t batch,
+                   unsigned flags, double* times_ms) {
+  return guarded([&] {
+    check(ctx);
+    if (m < 0 || n < 0 || nnz < 0) throw InvalidArg("invalid CSR: negative dimension");
+    if (n != x_rows) throw InvalidArg("run_spmm: A.n != X.rows");
+    if (d < 1) throw InvalidArg("run_spmm: X.cols must be >= 1");
+    if (!row_ptr || (!x && n > 0) || (!y && m > 0) || (nnz > 0 && (!col || !vals)))
+      throw InvalidArg("run_spmm: null array");
+    cudaEvent_t ev[5];
+    for (auto& e : ev) CUDA_CHECK(cudaEventCreate(&e));
+    cudaStream_t st = ctx->stream;
+    u64* d_rp = (u64*)ws_get(ctx, 0, ((size_t)m + 1) * 8);
+    uint32_t* d_col = (uint32_t*)ws_get(ctx, 1, (size_t)nnz * 4);
+    float* d_vals = (float*)ws_get(ctx, 2, (size_t)nnz * 4);
+    float* d_x = (float*)ws_get(ctx, 3, (size_t)n * (size_t)d * 4);
+    float* d_y = (float*)ws_get(ctx, 4, (size_t)m * (size_t)d * 4);
+    spmx_csr a;
+    a.ctx = ctx;
+    a.m = m;
+    a.n = n;
+    a.nnz = nnz;
+    a.row_ptr = d_rp;
+    a.col = d_col;
+    a.vals = d_vals;
+    spmx_plan* plan = nullptr;
+    try {
+      CUDA_CHECK(cudaEventRecord(ev[0], st));
+      CUDA_CHECK(cudaMemcpyAsync(d_rp, row_ptr, ((size_t)m + 1) * 8, cudaMemcpyHostToDevice, st));
+      if (nnz) {
+        CUDA_CHECK(cudaMemcpyAsync(d_col, col, (size_t)nnz * 4, cudaMemcpyHostToDevice, st));
+        CUDA_CHECK(cudaMemcpyAsync(d_vals, vals, (size_t)nnz * 4, cudaMemcpyHostToDevice, st));
+      }
+      CUDA_CHECK(cudaMemcpyAsync(d_x, x, (size_t)n * (size_t)d * 4, cudaMemcpyHostToDevice, st));
+      CUDA_CHECK(cudaEventRecord(ev[1], st));
+      validate_on_device(ctx, &a);
+      plan = plan_build(ctx, &a, strategy, parts, dynamic, batch, flags);
+      CUDA_CHECK(cudaEventRecord(ev[2], st));
+      run_kernels(ctx, plan, &a, d_x, d, d_y);
+      CUDA_CHECK(cudaEventRecord(ev[3], st));
+      CUDA_CHECK(cudaMemcpyAsync(y, d_y, (size_t)m * (size_t)d * 4, cudaMemcpyDeviceToHost, st));
+      CUDA_CHECK(cudaEventRecord(ev[4], st));
+      CUDA_CHECK(cudaStreamSynchronize(st));
+      if (times_ms) {
+        float t;
+        for (int i = 0; i < 4; ++i) {
+          CUDA_CHECK(cudaEventElapsedTime(&t, ev[i], ev[i + 1]));
+          times_ms[i] = t;
+        }
+        CUDA_CHECK(cudaEventElapsedTime(&t, ev[0], ev[4]));
+        times_ms[4] = t;
+        times_ms[5] = 0.0;
+      }
+    } catch (...) {
+      if (plan) plan_free(plan);
+      a.magic = 0;
+      for (auto& e : ev) cudaEventDestroy(e);
+      throw;
+    }
+    plan_free(plan);
+    a.magic = 0;
+    for (auto& e : ev) cudaEventDestroy(e);
+  });
+}
+
+int spmx_checksum_device(spmx_ctx* ctx, const float* d_y, size_t count, uint64_t* out) {
+  return guarded([&] {
+    check(ctx);
+    std::vector<float> h(count);
+    CUDA_CHECK(cudaMemcpyAsync(h.data(), d_y, count * 4, cudaMemcpyDeviceToHost, ctx->stream));
+    CUDA_CHECK(cudaStreamSynchronize(ctx->stream));
+    // FNV-1a-64 over the little-endian f32 bytes, dense.cpp:17-28
+    uint64_t hsh = 0xcbf29ce484222325ull;
+    for (size_t i = 0; i < count; ++i) {
+      uint32_t bits;
+      std::memcpy(&bits, &h[i], 4);
+      for (int s = 0; s < 32; s += 8) {
+        hsh ^= (bits >> s) & 0xffu;
+        hsh *= 0x100000001b3ull;
+      }
+    }
+    *out = hsh;
+  });
+}
+
+}  // extern "C"

@@ -1,0 +1,201 @@
+// spmx_partition.cuh — the reference's workload partitioner on the device.
+//
+// Every boundary is computed independently by one thread with the reference's own
+// integer arithmetic, so the result is bit-exact with src/partition.cpp run serially
+// (the reference's running `max(prev, r)` clamps are no-ops for a valid CSR because
+// targets, and therefore the search results, are nondecreasing in t; a CSR that
+// breaks that is rejected at upload by validate_csr_kernel).
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+namespace spmx_dev {
+
+typedef unsigned long long u64;
+
+// split_rows_static, src/partition.cpp:17-27: boundary t = t*base + min(t, rem).
+__global__ void row_boundaries_kernel(u64 m, unsigned parts, u64* __restrict__ bnd) {
+  const u64 t = (u64)blockIdx.x * blockDim.x + threadIdx.x;
+  if (t > parts) return;
+  const u64 base = m / parts, rem = m % parts;
+  bnd[t] = t * base + (t < rem ? t : rem);
+}
+
+// first index in a[0..count) with a[idx] >= target (std::lower_bound)
+__device__ __forceinline__ u64 lower_bound_dev(const u64* __restrict__ a, u64 count, u64 target) {
+  u64 lo = 0, hi = count;
+  while (lo < hi) {
+    const u64 mid = lo + (hi - lo) / 2;
+    if (__ldg(a + mid) < target)
+      lo = mid + 1;
+    else
+      hi = mid;
+  }
+  return lo;
+}
+
+// split_nnz, src/partition.cpp:35-51: boundary t (1 <= t < T) is the first row r with
+// row_ptr[r] >= ceil(t*nnz/T), searched over all m+1 entries and clamped to m.
+__global__ void nnz_boundaries_kernel(const u64* __restrict__ row_ptr, u64 m, u64 nnz,
+                                      unsigned parts, u64* __restrict__ bnd) {
+  const u64 t = (u64)blockIdx.x * blockDim.x + threadIdx.x;
+  if (t > parts) return;
+  if (t == 0) { bnd[0] = 0; return; }
+  if (t == parts) { bnd[t] = m; return; }
+  const u64 target = (t * nnz + parts - 1) / parts;  // same u64 arithmetic as partition.cpp:42
+  u64 r = lower_bound_dev(row_ptr, m + 1, target);
+  bnd[t] = r < m ? r : m;
+}
+
+// merge_path_search, src/partition.cpp:53-67. row_end[r] == row_ptr[r+1].
+__device__ __forceinline__ void merge_search_dev(const u64* __restrict__ row_ptr, u64 m, u64 nnz,
+                                                 u64 k, u64& out_i, u64& out_j) {
+  const u64* __restrict__ row_end = row_ptr + 1;
+  u64 lo = k > nnz ? k - nnz : 0;
+  u64 hi = k < m ? k : m;
+  while (lo < hi) {
+    const u64 mid = lo + (hi - lo) / 2;
+    if (__ldg(row_end + mid) <= k - mid - 1)
+      lo = mid + 1;
+    else
+      hi = mid;
+  }
+  out_i = lo;
+  out_j = k - lo;
+}
+
+__global__ void merge_search_kernel(const u64* __restrict__ row_ptr, u64 m, u64 nnz,
+                                    const u64* __restrict__ diag, u64 n_diag,
+                                    u64* __restrict__ out_i, u64* __restrict__ out_j) {
+  const u64 t = (u64)blockIdx.x * blockDim.x + threadIdx.x;
+  if (t >= n_diag) return;
+  u64 i, j;
+  merge_search_dev(row_ptr, m, nnz, diag[t], i, j);
+  out_i[t] = i;
+  out_j[t] = j;
+}
+
+// split_merge, src/partition.cpp:69-84: diagonal ceil(t*(m+nnz)/T); keep .i (row-snapped).
+// With snapped == 0 the diagonal itself is returned instead (true merge-path split).
+__global__ void merge_boundaries_kernel(const u64* __restrict__ row_ptr, u64 m, u64 nnz,
+                                        unsigned parts, int snapped, u64* __restrict__ out) {
+  const u64 t = (u64)blockIdx.x * blockDim.x + threadIdx.x;
+  if (t > parts) return;
+  if (t == 0) { out[0] = 0; return; }
+  if (t == parts) { out[t] = snapped ? m : m + nnz; return; }
+  const u64 k = (t * (m + nnz) + parts - 1) / parts;  // partition.cpp:76
+  if (!snapped) { out[t] = k; return; }
+  u64 i, j;
+  merge_search_dev(row_ptr, m, nnz, k, i, j);
+  out[t] = i;
+}
+
+// RowRange list from T+1 boundaries: out[2t] = bnd[t], out[2t+1] = bnd[t+1].
+__global__ void ranges_from_boundaries_kernel(const u64* __restrict__ bnd, unsigned parts,
+                                              u64* __restrict__ out) {
+  const u64 t = (u64)blockIdx.x * blockDim.x + threadIdx.x;
+  if (t >= parts) return;
+  out[2 * t] = bnd[t];
+  out[2 * t + 1] = bnd[t + 1];
+}
+
+// Row boundary b -> the merge-path diagonal through (b, row_ptr[b]).
+__global__ void boundaries_to_diagonals_kernel(const u64* __restrict__ row_ptr,
+                                               const u64* __restrict__ bnd, u64 count,
+                                               u64* __restrict__ diag) {
+  const u64 t = (u64)blockIdx.x * blockDim.x + threadIdx.x;
+  if (t >= count) return;
+  const u64 b = bnd[t];
+  diag[t] = b + __ldg(row_ptr + b);
+}
+
+// Work-list refinement: a strategy range of `items` merge items becomes
+// max(1, ceil(items / chunk_items)) chunks.
+__global__ void count_chunks_kernel(const u64* __restrict__ diag, u64 parts, u64 chunk_items,
+                                    u64* __restrict__ cnt) {
+  const u64 t = (u64)blockIdx.x * blockDim.x + threadIdx.x;
+  if (t >= parts) return;
+  const u64 items = diag[t + 1] - diag[t];
+  const u64 c = (items + chunk_items - 1) / chunk_items;
+  cnt[t] = c ? c : 1;
+}
+
+// Exclusive scan of cnt[0..n) into off[0..n], off[n] = total. One CTA; n is at most a
+// few million and this runs once per plan, outside any timed region.
+__global__ void exclusive_scan_kernel(const u64* __restrict__ cnt, u64 n, u64* __restrict__ off) {
+  __shared__ u64 part[1024];
+  const u64 per = (n + blockDim.x - 1) / blockDim.x;
+  const u64 lo = min((u64)threadIdx.x * per, n), hi = min(lo + per, n);
+  u64 s = 0;
+  for (u64 i = lo; i < hi; ++i) s += cnt[i];
+  part[threadIdx.x] = s;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    u64 run = 0;
+    for (unsigned i = 0; i < blockDim.x; ++i) {
+      const u64 v = part[i];
+      part[i] = run;
+      run += v;
+    }
+    off[n] = run;
+  }
+  __syncthreads();
+  u64 run = part[threadIdx.x];
+  for (u64 i = lo; i < hi; ++i) {
+    off[i] = run;
+    run += cnt[i];
+  }
+}
+
+// Chunk c belongs to range t = upper_bound(off, c) - 1 and is its s-th piece; its
+// starting diagonal is diag[t] + floor(s * items / cnt) (even split of the range).
+__global__ void chunk_diagonals_kernel(const u64* __restrict__ diag, const u64* __restrict__ off,
+                                       u64 parts, u64 n_chunks, u64* __restrict__ cdiag) {
+  const u64 c = (u64)blockIdx.x * blockDim.x + threadIdx.x;
+  if (c > n_chunks) return;
+  if (c == n_chunks) { cdiag[c] = diag[parts]; return; }
+  u64 lo = 0, hi = parts;  // last t with off[t] <= c
+  while (lo + 1 < hi) {
+    const u64 mid = lo + (hi - lo) / 2;
+    if (off[mid] <= c) lo = mid; else hi = mid;
+  }
+  const u64 t = lo, s = c - off[t], cnt = off[t + 1] - off[t];
+  const u64 items = diag[t + 1] - diag[t];
+  // s < cnt <= items/chunk+1: s*items fits u64 for any realistic size (items < 2^40, cnt < 2^24)
+  cdiag[c] = diag[t] + (s * items) / cnt;
+}
+
+// validate_csr, src/csr.cpp:18-42, on the device. err receives the largest code seen:
+// 2 row_ptr[0] != 0, 3 row_ptr[m] != nnz, 4 row_ptr decreasing, 5 column out of range.
+__global__ void validate_csr_kernel(const u64* __restrict__ row_ptr, const unsigned* __restrict__ col,
+                                    u64 m, u64 n, u64 nnz, int* err) {
+  const u64 stride = (u64)gridDim.x * blockDim.x;
+  const u64 tid = (u64)blockIdx.x * blockDim.x + threadIdx.x;
+  int e = 0;
+  if (tid == 0) {
+    if (row_ptr[0] != 0) e = 2;
+    if (row_ptr[m] != nnz) e = max(e, 3);
+  }
+  for (u64 i = tid; i < m; i += stride)
+    if (row_ptr[i + 1] < row_ptr[i] || row_ptr[i + 1] > nnz) e = max(e, 4);
+  for (u64 k = tid; k < nnz; k += stride)
+    if ((u64)col[k] >= n) e = max(e, 5);
+  if (e) atomicMax(err, e);
+}
+
+// next_batch, src/partition.cpp:29-33, one claim per thread on a shared device counter.
+__global__ void next_batch_claims_kernel(u64* counter, u64 batch, u64 m, u64 n_claims,
+                                         u64* __restrict__ out) {
+  const u64 t = (u64)blockIdx.x * blockDim.x + threadIdx.x;
+  if (t >= n_claims) return;
+  const u64 v = atomicAdd(counter, batch);
+  if (v >= m) {
+    out[2 * t] = out[2 * t + 1] = ~0ull;
+  } else {
+    out[2 * t] = v;
+    out[2 * t + 1] = v + batch < m ? v + batch : m;
+  }
+}
+
+}  // namespace spmx_dev

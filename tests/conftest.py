@@ -1,0 +1,53 @@
+import os
+import sys
+
+import numpy as np
+import pytest
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+if ROOT not in sys.path:
+    sys.path.insert(0, ROOT)
+
+GOLDEN = os.path.join(ROOT, "tests", "golden")
+
+
+def pytest_configure(config):
+    config.addinivalue_line("markers", "gpu: needs a CUDA device (run on the B200 box)")
+
+
+@pytest.fixture(scope="session")
+def oracle():
+    """The CPU restatement (oracle/spmx_oracle.c) — the checker, never the product."""
+    from oracle.pyoracle import Oracle
+    return Oracle()
+
+
+@pytest.fixture(scope="session")
+def reflib():
+    """The unmodified reference library, where oracle/_ref was built (optional)."""
+    from oracle.pyoracle import RefLib
+    if not RefLib.available():
+        pytest.skip("oracle/_ref/libspmx_ref.so not built here")
+    return RefLib()
+
+
+@pytest.fixture(scope="session")
+def golden_instances():
+    z = np.load(os.path.join(GOLDEN, "ref_instances.npz"))
+    n = len([k for k in z.files if k.endswith("_dims")])
+    out = []
+    for i in range(n):
+        p = f"i{i}_"
+        out.append({k[len(p):]: z[k] for k in z.files if k.startswith(p)})
+    return out
+
+
+@pytest.fixture(scope="session")
+def ctx():
+    """A context on cuda:0 through the C ABI. Fails loudly (no CPU fallback)."""
+    import torch
+    assert torch.cuda.is_available(), "gpu tests need a CUDA device"
+    from paper_2312_05639_b200.binding import Context
+    c = Context(0)
+    yield c
+    c.close()
