@@ -16,7 +16,8 @@ import numpy as np
 
 _PKG = os.path.dirname(os.path.abspath(__file__))
 _ROOT = os.path.dirname(_PKG)
-LIB_PATH = os.path.join(_PKG, "libspmx_b200.so")
+# SPMX_B200_LIB selects another build of the same library (kernel-tuning experiments only)
+LIB_PATH = os.environ.get("SPMX_B200_LIB") or os.path.join(_PKG, "libspmx_b200.so")
 CSRC = os.path.join(_PKG, "csrc")
 HEADER = os.path.join(_ROOT, "include", "spmx_b200.h")
 

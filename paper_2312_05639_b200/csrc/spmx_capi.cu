@@ -208,6 +208,14 @@ void launch_one(const spmx_plan* p, const spmx_dev::SpmmArgs& args, cudaStream_t
     const unsigned grid =
         (unsigned)((args.n_chunks + spmx_dev::kWarpsPerCta - 1) / spmx_dev::kWarpsPerCta);
     if (grid == 0) return;
+#ifdef SPMX_CARVEOUT
+    static bool once = false;
+    if (!once) {
+      once = true;
+      CUDA_CHECK(cudaFuncSetAttribute(spmx_dev::spmm_chunk_kernel<D_CT, G, VEC, NT, RAGGED>,
+                                      cudaFuncAttributePreferredSharedMemoryCarveout, SPMX_CARVEOUT));
+    }
+#endif
     spmx_dev::spmm_chunk_kernel<D_CT, G, VEC, NT, RAGGED>
         <<<grid, spmx_dev::kWarpsPerCta * 32, 0, st>>>(args);
   }
@@ -280,12 +288,15 @@ void run_kernels(spmx_ctx* ctx, const spmx_plan* p, const spmx_csr* a, const flo
     args.c0 = (int)c0;
     args.dw = dw;
     if (p->dynamic) CUDA_CHECK(cudaMemsetAsync(p->counter, 0, sizeof(u64), ctx->stream));
+#ifndef SPMX_NT
+#define SPMX_NT 2  // float4 tiles per lane for the specialised widths
+#endif
     if (vec == 4 && c0 == 0 && d == 32) {
-      launch_one<32, 8, 4, 1, false>(p, args, ctx->stream, ctx->sm_count);
+      launch_one<32, 8 / SPMX_NT, 4, SPMX_NT, false>(p, args, ctx->stream, ctx->sm_count);
     } else if (vec == 4 && c0 == 0 && d == 64) {
-      launch_one<64, 16, 4, 1, false>(p, args, ctx->stream, ctx->sm_count);
+      launch_one<64, 16 / SPMX_NT, 4, SPMX_NT, false>(p, args, ctx->stream, ctx->sm_count);
     } else if (vec == 4 && c0 == 0 && d == 128) {
-      launch_one<128, 32, 4, 1, false>(p, args, ctx->stream, ctx->sm_count);
+      launch_one<128, 32 / SPMX_NT, 4, SPMX_NT, false>(p, args, ctx->stream, ctx->sm_count);
     } else {
       const int lanes = (dw + vec - 1) / vec;
       int g = pow2_ceil(std::min(lanes, 32));
