@@ -60,7 +60,10 @@ int guarded(F&& f) {
 
 constexpr uint32_t kMagicCtx = 0x58435443, kMagicCsr = 0x58435352, kMagicPlan = 0x58504c4e;
 constexpr u64 kDefaultChunkItems = 1024;  // merge items (rows + nonzeros) per warp-level chunk
-constexpr unsigned kDefaultLongSeg = 64;  // row segments >= this are shared by the warp's groups
+#ifndef SPMX_LONG_SEG
+#define SPMX_LONG_SEG 256
+#endif
+constexpr unsigned kDefaultLongSeg = SPMX_LONG_SEG;  // row segments >= this are shared by the warp's groups
 
 inline unsigned blocks_for(u64 n, unsigned threads = 256) {
   return (unsigned)((n + threads - 1) / threads);
@@ -208,14 +211,20 @@ void launch_one(const spmx_plan* p, const spmx_dev::SpmmArgs& args, cudaStream_t
     const unsigned grid =
         (unsigned)((args.n_chunks + spmx_dev::kWarpsPerCta - 1) / spmx_dev::kWarpsPerCta);
     if (grid == 0) return;
-#ifdef SPMX_CARVEOUT
-    static bool once = false;
-    if (!once) {
-      once = true;
+#ifndef SPMX_CARVEOUT
+#define SPMX_CARVEOUT 25  // % of the unified L1/shared array given to shared memory
+#endif
+    // In-flight X-row gathers are held in L1 lines: the kernel needs only a few KB of shared
+    // memory, so keep the carve-out small (the driver's default picked 135 KB, leaving the
+    // gathers half the L1; tools/microbench/gather_bw2.cu shows the effect).
+    static std::atomic<uint64_t> done_mask{0};  // one bit per device
+    int dev = 0;
+    CUDA_CHECK(cudaGetDevice(&dev));
+    if (!(done_mask.load() >> (dev & 63) & 1)) {
+      done_mask.fetch_or(1ull << (dev & 63));
       CUDA_CHECK(cudaFuncSetAttribute(spmx_dev::spmm_chunk_kernel<D_CT, G, VEC, NT, RAGGED>,
                                       cudaFuncAttributePreferredSharedMemoryCarveout, SPMX_CARVEOUT));
     }
-#endif
     spmx_dev::spmm_chunk_kernel<D_CT, G, VEC, NT, RAGGED>
         <<<grid, spmx_dev::kWarpsPerCta * 32, 0, st>>>(args);
   }

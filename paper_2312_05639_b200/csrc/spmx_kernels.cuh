@@ -117,7 +117,7 @@ __device__ __forceinline__ void zero_acc(float (&acc)[NT][VEC]) {
 constexpr int kWindowRows = 128;  // rows whose bounds a warp stages at a time
 
 #ifndef SPMX_U
-#define SPMX_U 8
+#define SPMX_U 16  // LDG.128 gathers in flight per lane (measured best with 2 CTAs/SM)
 #endif
 
 // Per-warp shared memory.
@@ -319,8 +319,14 @@ __device__ __forceinline__ void process_piece(const SpmmArgs& a, u64 r0, u64 j0,
                   acc[tt][e] = __fmaf_rn(vq, xv[u][tt].v[e], acc[tt][e]);
               }
           }
+#ifdef SPMX_EXP_NOROWEND
+          if (false) {
+#else
           if (--left == 0) {  // row k ends here: store it, start the next one
+#endif
+#ifndef SPMX_EXP_NOSTORE
             store_row<G, VEC, NT, RAGGED>(a, ybase + (size_t)sm.row_idx[k] * (size_t)ldx, lg, acc);
+#endif
             zero_acc(acc);
             ++k;
             left = (k < k1) ? sm.row_end[k] - sm.row_end[k - 1] : 0x7fffffffu;
@@ -366,7 +372,7 @@ __device__ __forceinline__ void process_piece(const SpmmArgs& a, u64 r0, u64 j0,
 }
 
 #ifndef SPMX_MIN_CTAS
-#define SPMX_MIN_CTAS 3
+#define SPMX_MIN_CTAS 2
 #endif
 
 // Static work list: warp w of the grid owns chunk w.
