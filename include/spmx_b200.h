@@ -137,6 +137,15 @@ int spmx_spmm_host(spmx_ctx* ctx, int64_t m, int64_t n, int64_t nnz, const uint6
                    int64_t d, float* y, int strategy, unsigned parts, int dynamic, uint64_t batch,
                    unsigned flags, double* times_ms);
 
+/* ---- verification, on the device (RunConfig.verify, executor.cpp:110) ------------------------
+ * spmm_reference (reference.cpp:10-25, Alg. 1): one thread per output element, multiply then
+ * add with two roundings, CSR order — bitwise equal to the reference's serial loop. */
+int spmx_spmm_reference(spmx_ctx* ctx, const spmx_csr* a, const float* d_x, int64_t x_rows,
+                        int64_t d, float* d_y);
+/* max_relative_error (executor.cpp:27-34): max_i |y_i - ref_i| / max(|ref_i|, 1e-6) */
+int spmx_max_relative_error(spmx_ctx* ctx, const float* d_y, const float* d_ref, size_t count,
+                            double* out);
+
 /* ---- helpers for the reference's report fields ---------------------------------------------- */
 /* checksum(Y), dense.cpp:17-28, of a device buffer (FNV-1a is sequential: the buffer is copied
  * to the host and hashed there; a reporting helper, not on the hot path) */

@@ -113,6 +113,8 @@ class Lib:
         L.spmx_spmm_host.argtypes = [vp, i64, i64, i64, vp, vp, vp, vp, i64, i64, vp, C.c_int,
                                      C.c_uint, C.c_int, u64, C.c_uint, P(C.c_double)]
         L.spmx_checksum_device.argtypes = [vp, vp, sz, P(u64)]
+        L.spmx_spmm_reference.argtypes = [vp, vp, vp, i64, i64, vp]
+        L.spmx_max_relative_error.argtypes = [vp, vp, vp, sz, P(C.c_double)]
 
     def check(self, rc: int):
         if rc == 0:
@@ -263,6 +265,17 @@ class Context:
                                                _ptr(vals) if vals.size else 0, _ptr(x), x_rows, d,
                                                _ptr(y), s, parts, int(dynamic), batch, flags, t))
         return y, dict(h2d=t[0], plan=t[1], kernel=t[2], d2h=t[3], total=t[4])
+
+    def spmm_reference(self, a: "DeviceCsr", x, y):
+        """spmm_reference (unfused Alg. 1) on the device, for verification."""
+        self.L.check(self.L.lib.spmx_spmm_reference(self.h, a.h, _ptr(x), x.shape[0], x.shape[1],
+                                                    _ptr(y)))
+
+    def max_relative_error(self, y, ref) -> float:
+        out = C.c_double()
+        self.L.check(self.L.lib.spmx_max_relative_error(self.h, _ptr(y), _ptr(ref), y.numel(),
+                                                        C.byref(out)))
+        return out.value
 
     def checksum(self, y) -> int:
         out = C.c_uint64()

@@ -829,6 +829,40 @@ int spmx_spmm_host(spmx_ctx* ctx, int64_t m, int64_t n, int64_t nnz, const uint6
   });
 }
 
+int spmx_spmm_reference(spmx_ctx* ctx, const spmx_csr* a, const float* d_x, int64_t x_rows,
+                        int64_t d, float* d_y) {
+  return guarded([&] {
+    check(ctx);
+    check(a);
+    if (a->n != x_rows) throw InvalidArg("spmm_reference: A.n != X.rows");  // reference.cpp:11
+    if (d < 1) throw InvalidArg("spmm_reference: X.cols must be >= 1");
+    const u64 total = (u64)a->m * (u64)d;
+    if (total == 0) return;
+    spmx_dev::spmm_unfused_reference_kernel<<<blocks_for(total), 256, 0, ctx->stream>>>(
+        a->row_ptr, a->col, a->vals, d_x, d_y, (u64)a->m, (int)d);
+    post_launch();
+  });
+}
+
+int spmx_max_relative_error(spmx_ctx* ctx, const float* d_y, const float* d_ref, size_t count,
+                            double* out) {
+  return guarded([&] {
+    check(ctx);
+    unsigned long long* d_bits = dev_alloc<unsigned long long>(1);
+    CUDA_CHECK(cudaMemsetAsync(d_bits, 0, 8, ctx->stream));
+    if (count) {
+      const unsigned nb = (unsigned)std::min<u64>((u64)ctx->sm_count * 8, (count + 255) / 256);
+      spmx_dev::max_rel_err_kernel<<<nb, 256, 0, ctx->stream>>>(d_y, d_ref, (u64)count, d_bits);
+      post_launch();
+    }
+    unsigned long long bits = 0;
+    CUDA_CHECK(cudaMemcpyAsync(&bits, d_bits, 8, cudaMemcpyDeviceToHost, ctx->stream));
+    CUDA_CHECK(cudaStreamSynchronize(ctx->stream));
+    CUDA_CHECK(cudaFree(d_bits));
+    std::memcpy(out, &bits, 8);
+  });
+}
+
 int spmx_checksum_device(spmx_ctx* ctx, const float* d_y, size_t count, uint64_t* out) {
   return guarded([&] {
     check(ctx);

@@ -437,4 +437,37 @@ __global__ void carry_fixup_kernel(const u64* __restrict__ row_ptr,
   }
 }
 
+// spmm_reference (src/reference.cpp:10-25, Alg. 1) for RunConfig.verify: one thread per
+// output element, ret += v * x with separate multiply and add (two roundings), CSR order.
+__global__ void spmm_unfused_reference_kernel(const u64* __restrict__ row_ptr,
+                                              const u32* __restrict__ col,
+                                              const float* __restrict__ vals,
+                                              const float* __restrict__ x, float* __restrict__ y,
+                                              u64 m, int d) {
+  const u64 idx = (u64)blockIdx.x * blockDim.x + threadIdx.x;
+  if (idx >= m * (u64)d) return;
+  const u64 i = idx / (u64)d;
+  const int j = (int)(idx % (u64)d);
+  float ret = 0.0f;
+  for (u64 k = row_ptr[i]; k < row_ptr[i + 1]; ++k)
+    ret = __fadd_rn(ret, __fmul_rn(vals[k], x[(size_t)col[k] * d + j]));
+  y[idx] = ret;
+}
+
+// max_relative_error (src/executor.cpp:27-34). The maximum of non-negative doubles is taken
+// with an integer atomicMax on the bit pattern (order-preserving for non-negative values).
+__global__ void max_rel_err_kernel(const float* __restrict__ y, const float* __restrict__ ref,
+                                   u64 count, unsigned long long* out_bits) {
+  double worst = 0.0;
+  for (u64 i = (u64)blockIdx.x * blockDim.x + threadIdx.x; i < count;
+       i += (u64)gridDim.x * blockDim.x) {
+    const double r = (double)ref[i];
+    const double denom = fmax(fabs(r), 1e-6);
+    const double e = fabs((double)y[i] - r) / denom;
+    worst = (e > worst || e != e) ? e : worst;
+  }
+  if (worst != worst) worst = __longlong_as_double(0x7ff0000000000000ll);  // NaN -> +inf
+  atomicMax(out_bits, (unsigned long long)__double_as_longlong(worst));
+}
+
 }  // namespace spmx_dev

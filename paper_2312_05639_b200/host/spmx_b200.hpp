@@ -1,0 +1,360 @@
+// spmx_b200.hpp — C++ host mirror of the reference's public API for the SpMM path, over the
+// C ABI of libspmx_b200.so (include/spmx_b200.h). Header-only; link with -lspmx_b200.
+//
+// Same names, argument meaning and error behaviour as the reference (namespace spmx,
+// /root/reference/proj/include/spmx/{csr,dense,partition,executor}.hpp), so code written
+// against the reference — including its tests — compiles against this header unchanged for
+// the path in scope:
+//     CsrMatrix, DenseMatrix, Strategy, RowRange, WorkPartition, MergeCoordinate,
+//     split_rows_static, split_nnz, split_merge, merge_path_search, make_partition,
+//     RunConfig, RunReport, run_spmm, max_relative_error, checksum, kVerifyTolerance.
+// Differences, all forced by the device:
+//   * the work runs on a B200 through hand-written CUDA kernels; there is no CPU fallback;
+//   * RunConfig.threads is the number of partition ranges T (0 = a default that fills the
+//     GPU), not OS threads; RunReport.threads echoes it;
+//   * Backend::Native is the default device mode (ranges heavier than a chunk and the merge
+//     strategy split rows at nonzero granularity; deterministic, within the reference's
+//     1e-5 verify tolerance); Backend::Interp — the reference's bitwise oracle — selects
+//     SPMX_EXACT_ORDER, whose result is bitwise equal to the reference's for every
+//     strategy and T;
+//   * codegen_s reports the plan construction (device partitioner + work list), the step
+//     that — like the reference's code generation — happens once before the timed trials;
+//   * tier_cap and collect_counters are accepted and ignored (x86-only concepts).
+#pragma once
+
+#include <algorithm>
+#include <cstdint>
+#include <cstring>
+#include <optional>
+#include <stdexcept>
+#include <string>
+#include <utility>
+#include <vector>
+
+#include "../../include/spmx_b200.h"
+
+namespace spmx {
+
+// ---- data model (csr.hpp:10-20, dense.hpp:9-21) -----------------------------------------
+struct CsrMatrix {
+  int64_t m = 0, n = 0, nnz = 0;
+  std::vector<uint64_t> row_ptr;
+  std::vector<uint32_t> col_indices;
+  std::vector<float> vals;
+  uint64_t row_nnz(int64_t i) const { return row_ptr[size_t(i) + 1] - row_ptr[size_t(i)]; }
+  uint64_t max_row_nnz() const {
+    uint64_t best = 0;
+    for (int64_t i = 0; i < m; ++i) best = std::max(best, row_nnz(i));
+    return best;
+  }
+};
+
+struct DenseMatrix {
+  int64_t rows = 0, cols = 0;
+  std::vector<float> data;
+  DenseMatrix() = default;
+  DenseMatrix(int64_t r, int64_t c) : rows(r), cols(c), data(size_t(r) * size_t(c), 0.0f) {}
+  float& at(int64_t i, int64_t j) { return data[size_t(i) * size_t(cols) + size_t(j)]; }
+  float at(int64_t i, int64_t j) const { return data[size_t(i) * size_t(cols) + size_t(j)]; }
+  const float* row(int64_t i) const { return data.data() + size_t(i) * size_t(cols); }
+  float* row(int64_t i) { return data.data() + size_t(i) * size_t(cols); }
+};
+
+enum class Strategy { RowSplit, NnzSplit, MergeSplit };
+inline const char* strategy_name(Strategy s) {
+  return s == Strategy::RowSplit ? "row" : s == Strategy::NnzSplit ? "nnz" : "merge";
+}
+
+struct RowRange {
+  uint64_t begin = 0, end = 0;
+  uint64_t size() const { return end - begin; }
+  bool operator==(const RowRange&) const = default;
+};
+struct DispatchConfig {
+  uint64_t batch_size = 128;
+};
+struct WorkPartition {
+  Strategy strategy = Strategy::RowSplit;
+  std::vector<RowRange> ranges;  // empty under dynamic dispatch
+  std::optional<DispatchConfig> dynamic;
+};
+struct MergeCoordinate {
+  uint64_t i = 0, j = 0;
+};
+
+namespace detail {
+
+// status code -> the reference's exception type
+inline void check(int rc) {
+  if (rc == SPMX_OK) return;
+  const std::string msg = spmx_last_error();
+  if (rc == SPMX_EINVAL) throw std::invalid_argument(msg);
+  if (rc == SPMX_ELOGIC) throw std::logic_error(msg);
+  throw std::runtime_error(msg);
+}
+
+inline int to_c(Strategy s) {
+  return s == Strategy::RowSplit ? SPMX_ROW_SPLIT
+                                 : s == Strategy::NnzSplit ? SPMX_NNZ_SPLIT : SPMX_MERGE_SPLIT;
+}
+
+// RAII over the opaque handles
+struct Ctx {
+  spmx_ctx* h = nullptr;
+  explicit Ctx(int device = 0) { check(spmx_ctx_create(device, nullptr, &h)); }
+  ~Ctx() { if (h) spmx_ctx_destroy(h); }
+  Ctx(const Ctx&) = delete;
+  Ctx& operator=(const Ctx&) = delete;
+};
+struct DevCsr {
+  spmx_csr* h = nullptr;
+  DevCsr(Ctx& c, const CsrMatrix& a) {
+    if (a.row_ptr.size() != size_t(a.m) + 1)
+      throw std::invalid_argument("invalid CSR: row_ptr length != m+1");
+    if (a.col_indices.size() != size_t(a.nnz) || a.vals.size() != size_t(a.nnz))
+      throw std::invalid_argument("invalid CSR: col_indices/vals length != nnz");
+    check(spmx_csr_upload(c.h, a.m, a.n, a.nnz, a.row_ptr.data(), a.col_indices.data(),
+                          a.vals.data(), &h));
+  }
+  // structure only (partition functions never read columns or values)
+  DevCsr(Ctx& c, int64_t m, int64_t nnz, const uint64_t* row_ptr) {
+    std::vector<uint32_t> col(size_t(nnz), 0u);
+    std::vector<float> vals(size_t(nnz), 0.0f);
+    check(spmx_csr_upload(c.h, m, 1, nnz, row_ptr, col.data(), vals.data(), &h));
+  }
+  ~DevCsr() { if (h) spmx_csr_destroy(h); }
+  DevCsr(const DevCsr&) = delete;
+  DevCsr& operator=(const DevCsr&) = delete;
+};
+struct DevBuf {
+  Ctx& c;
+  void* p = nullptr;
+  DevBuf(Ctx& ctx, size_t bytes) : c(ctx) { check(spmx_dev_alloc(c.h, bytes, &p)); }
+  ~DevBuf() { if (p) spmx_dev_free(c.h, p); }
+  DevBuf(const DevBuf&) = delete;
+  DevBuf& operator=(const DevBuf&) = delete;
+};
+struct Plan {
+  spmx_plan* h = nullptr;
+  ~Plan() { if (h) spmx_plan_destroy(h); }
+};
+
+inline std::vector<RowRange> to_ranges(const std::vector<uint64_t>& flat) {
+  std::vector<RowRange> r(flat.size() / 2);
+  for (size_t t = 0; t < r.size(); ++t) r[t] = {flat[2 * t], flat[2 * t + 1]};
+  return r;
+}
+
+inline double now_s();
+
+}  // namespace detail
+
+// ---- partitioner (partition.hpp:44-68), computed on the device, bit-exact ----------------------
+inline std::vector<RowRange> split_rows_static(uint64_t m, unsigned threads) {
+  if (threads == 0) throw std::invalid_argument("split_rows_static: zero threads");
+  detail::Ctx c;
+  std::vector<uint64_t> flat(2 * size_t(threads));
+  detail::check(spmx_split_rows_static(c.h, m, threads, flat.data()));
+  return detail::to_ranges(flat);
+}
+
+inline std::vector<RowRange> split_nnz(const CsrMatrix& a, unsigned threads) {
+  if (threads == 0) throw std::invalid_argument("split_nnz: zero threads");
+  detail::Ctx c;
+  detail::DevCsr d(c, a.m, a.nnz, a.row_ptr.data());
+  std::vector<uint64_t> flat(2 * size_t(threads));
+  detail::check(spmx_split_nnz(c.h, d.h, threads, flat.data()));
+  return detail::to_ranges(flat);
+}
+
+inline std::vector<RowRange> split_merge(const CsrMatrix& a, unsigned threads) {
+  if (threads == 0) throw std::invalid_argument("split_merge: zero threads");
+  detail::Ctx c;
+  detail::DevCsr d(c, a.m, a.nnz, a.row_ptr.data());
+  std::vector<uint64_t> flat(2 * size_t(threads));
+  detail::check(spmx_split_merge(c.h, d.h, threads, flat.data()));
+  return detail::to_ranges(flat);
+}
+
+// row_end[r] == row_ptr[r+1], exactly as the reference takes it (partition.hpp:56-58);
+// row_end - 1 must therefore be the start of a row_ptr array of m+1 entries.
+inline MergeCoordinate merge_path_search(uint64_t k, const uint64_t* row_end, uint64_t m,
+                                         uint64_t nnz) {
+  if (k > m + nnz) throw std::invalid_argument("merge_path_search: diagonal out of range");
+  detail::Ctx c;
+  detail::DevCsr d(c, int64_t(m), int64_t(nnz), row_end - 1);
+  MergeCoordinate out;
+  detail::check(spmx_merge_path_search(c.h, d.h, 1, &k, &out.i, &out.j));
+  return out;
+}
+
+// many diagonals at once (one upload): the efficient form of the call above
+inline std::vector<MergeCoordinate> merge_path_search(const CsrMatrix& a,
+                                                      const std::vector<uint64_t>& ks) {
+  detail::Ctx c;
+  detail::DevCsr d(c, a.m, a.nnz, a.row_ptr.data());
+  std::vector<uint64_t> oi(ks.size()), oj(ks.size());
+  detail::check(spmx_merge_path_search(c.h, d.h, ks.size(), ks.data(), oi.data(), oj.data()));
+  std::vector<MergeCoordinate> out(ks.size());
+  for (size_t t = 0; t < ks.size(); ++t) out[t] = {oi[t], oj[t]};
+  return out;
+}
+
+inline WorkPartition make_partition(const CsrMatrix& a, Strategy strategy, unsigned threads,
+                                    bool dynamic_dispatch, uint64_t batch_size) {
+  if (threads == 0) throw std::invalid_argument("make_partition: zero threads");
+  WorkPartition p;
+  p.strategy = strategy;
+  if (dynamic_dispatch) {
+    if (strategy != Strategy::RowSplit)
+      throw std::invalid_argument("dynamic dispatch pairs with row-split only");
+    if (batch_size == 0) throw std::invalid_argument("batch_size must be >= 1");
+    p.dynamic = DispatchConfig{batch_size};
+    return p;
+  }
+  switch (strategy) {
+    case Strategy::RowSplit: p.ranges = split_rows_static(uint64_t(a.m), threads); break;
+    case Strategy::NnzSplit: p.ranges = split_nnz(a, threads); break;
+    case Strategy::MergeSplit: p.ranges = split_merge(a, threads); break;
+  }
+  return p;
+}
+
+// ---- executor (executor.hpp:20-50) ---------------------------------------------------------------------
+enum class Backend { Native, Interp };
+inline const char* backend_name(Backend b) { return b == Backend::Native ? "native" : "interp"; }
+enum class SimdTier { Scalar, V256, V512 };  // kept for source compatibility; unused on the GPU
+
+struct RunConfig {
+  Strategy strategy = Strategy::RowSplit;
+  bool dynamic_dispatch = true;  // RowSplit only
+  unsigned threads = 0;          // partition ranges T; 0 = fill the GPU
+  Backend backend = Backend::Native;
+  std::optional<SimdTier> tier_cap;
+  uint64_t batch_size = 128;
+  bool verify = false;
+  unsigned trials = 1;
+  bool collect_counters = false;
+  int device = 0;  // extension: which GPU
+};
+
+struct RunReport {
+  std::vector<double> times_s;  // device time of each trial (CUDA events)
+  double mean_s = 0.0;
+  double codegen_s = 0.0;  // plan construction
+  double gflops = 0.0;     // 2*nnz*d / mean_s / 1e9
+  SimdTier tier = SimdTier::Scalar;
+  unsigned threads = 0;
+  std::optional<double> max_rel_err;  // when verify is set
+  uint64_t n_chunks = 0;              // extension: size of the device work list
+};
+
+inline constexpr double kVerifyTolerance = 1e-5;
+
+// executor.cpp:27-34
+inline double max_relative_error(const DenseMatrix& y, const DenseMatrix& ref) {
+  if (y.data.size() != ref.data.size())
+    throw std::invalid_argument("max_relative_error: shape mismatch");
+  detail::Ctx c;
+  const size_t bytes = y.data.size() * sizeof(float);
+  detail::DevBuf dy(c, bytes), dr(c, bytes);
+  detail::check(spmx_h2d(c.h, dy.p, y.data.data(), bytes));
+  detail::check(spmx_h2d(c.h, dr.p, ref.data.data(), bytes));
+  double out = 0.0;
+  detail::check(spmx_max_relative_error(c.h, (const float*)dy.p, (const float*)dr.p,
+                                        y.data.size(), &out));
+  return out;
+}
+
+// dense.cpp:17-28: FNV-1a-64 over the little-endian f32 bytes (sequential by definition)
+inline uint64_t checksum(const DenseMatrix& y) {
+  uint64_t h = 0xcbf29ce484222325ull;
+  for (float f : y.data) {
+    uint32_t bits;
+    std::memcpy(&bits, &f, 4);
+    for (int s = 0; s < 32; s += 8) {
+      h ^= (bits >> s) & 0xffu;
+      h *= 0x100000001b3ull;
+    }
+  }
+  return h;
+}
+
+// reference.hpp:11 — Alg. 1 (unfused), evaluated on the device
+inline DenseMatrix spmm_reference(const CsrMatrix& a, const DenseMatrix& x) {
+  if (a.n != x.rows) throw std::invalid_argument("spmm_reference: A.n != X.rows");
+  detail::Ctx c;
+  detail::DevCsr da(c, a);
+  DenseMatrix y(a.m, x.cols);
+  detail::DevBuf dx(c, x.data.size() * 4), dy(c, y.data.size() * 4);
+  detail::check(spmx_h2d(c.h, dx.p, x.data.data(), x.data.size() * 4));
+  detail::check(spmx_spmm_reference(c.h, da.h, (const float*)dx.p, x.rows, x.cols, (float*)dy.p));
+  detail::check(spmx_d2h(c.h, y.data.data(), dy.p, y.data.size() * 4));
+  detail::check(spmx_ctx_synchronize(c.h));
+  return y;
+}
+
+// executor.hpp:44-45
+inline std::pair<DenseMatrix, RunReport> run_spmm(const CsrMatrix& a, const DenseMatrix& x,
+                                                  const RunConfig& cfg) {
+  // executor.cpp:38-46, same order and messages
+  if (a.n != x.rows) throw std::invalid_argument("run_spmm: A.n != X.rows");
+  if (cfg.trials < 1) throw std::invalid_argument("run_spmm: trials must be >= 1");
+  if (cfg.batch_size < 1) throw std::invalid_argument("run_spmm: batch_size must be >= 1");
+  if (cfg.dynamic_dispatch && cfg.strategy != Strategy::RowSplit)
+    throw std::invalid_argument("dynamic dispatch pairs with row-split only");
+  const bool dynamic = cfg.dynamic_dispatch && cfg.strategy == Strategy::RowSplit;
+  const unsigned flags = cfg.backend == Backend::Interp ? SPMX_EXACT_ORDER : 0u;
+
+  detail::Ctx c(cfg.device);
+  detail::DevCsr da(c, a);
+  const int64_t d = x.cols;
+  DenseMatrix y(a.m, d);
+  detail::DevBuf dx(c, x.data.size() * 4), dy(c, y.data.size() * 4);
+  detail::check(spmx_h2d(c.h, dx.p, x.data.data(), x.data.size() * 4));
+
+  RunReport report;
+  detail::Plan plan;
+  {
+    // plan once per run, before the timed trials (executor.cpp:54-62)
+    detail::check(spmx_ctx_synchronize(c.h));
+    const double t0 = detail::now_s();
+    detail::check(spmx_plan_create(c.h, da.h, detail::to_c(cfg.strategy), cfg.threads,
+                                   dynamic ? 1 : 0, cfg.batch_size, flags, &plan.h));
+    detail::check(spmx_ctx_synchronize(c.h));
+    report.codegen_s = detail::now_s() - t0;
+  }
+  unsigned parts = 0;
+  uint64_t chunks = 0;
+  detail::check(spmx_plan_info(plan.h, &parts, &chunks, nullptr));
+  report.threads = parts;
+  report.n_chunks = chunks;
+  for (unsigned trial = 0; trial < cfg.trials; ++trial) {
+    float ms = 0.0f;
+    detail::check(spmx_spmm(c.h, plan.h, da.h, (const float*)dx.p, x.rows, d, (float*)dy.p, &ms));
+    report.times_s.push_back(double(ms) * 1e-3);
+  }
+  double sum = 0.0;
+  for (double t : report.times_s) sum += t;
+  report.mean_s = sum / double(report.times_s.size());
+  report.gflops = report.mean_s > 0.0 ? 2.0 * double(a.nnz) * double(d) / report.mean_s / 1e9 : 0.0;
+  if (cfg.verify) {
+    detail::DevBuf dref(c, y.data.size() * 4);
+    detail::check(spmx_spmm_reference(c.h, da.h, (const float*)dx.p, x.rows, d, (float*)dref.p));
+    double e = 0.0;
+    detail::check(spmx_max_relative_error(c.h, (const float*)dy.p, (const float*)dref.p,
+                                          y.data.size(), &e));
+    report.max_rel_err = e;
+  }
+  detail::check(spmx_d2h(c.h, y.data.data(), dy.p, y.data.size() * 4));
+  detail::check(spmx_ctx_synchronize(c.h));
+  return {std::move(y), std::move(report)};
+}
+
+}  // namespace spmx
+
+#include <chrono>
+inline double spmx::detail::now_s() {
+  return std::chrono::duration<double>(std::chrono::steady_clock::now().time_since_epoch())
+      .count();
+}

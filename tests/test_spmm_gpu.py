@@ -251,3 +251,25 @@ def test_host_entry_point(ctx, oracle):
         ctx.spmm_host(m, n, rp, col, vals, rng.random((n + 1, d), np.float32))
     with pytest.raises(SpmxInvalidArgument):
         ctx.spmm_host(m, n, rp, col, vals, x, strategy="nnz", dynamic=True)
+
+
+def test_device_reference_and_error_metric(ctx, oracle):
+    """spmx_spmm_reference (Alg. 1 on the device, used by RunConfig.verify) is bitwise the
+    reference's unfused loop; spmx_max_relative_error equals executor.cpp:27-34."""
+    rng = np.random.default_rng(31)
+    m, n, d = 300, 200, 45
+    rp, col, vals = rand_csr(rng, m, n, 0.08)
+    x = (rng.random((n, d), np.float32) * 2 - 1).astype(np.float32)
+    a = ctx.csr_upload(m, n, rp, col, vals)
+    xd = torch.from_numpy(x).cuda()
+    yr = torch.empty(m, d, device="cuda")
+    ctx.spmm_reference(a, xd, yr)
+    ctx.synchronize()
+    want = oracle.spmm_unfused(m, n, rp, col, vals, x)
+    assert np.array_equal(yr.cpu().numpy().view(np.uint32), want.view(np.uint32))
+    p = ctx.plan(a, "merge")
+    y = torch.empty(m, d, device="cuda")
+    ctx.spmm(p, a, xd, y)
+    ctx.synchronize()
+    got = ctx.max_relative_error(y, yr)
+    assert got == oracle.max_relative_error(y.cpu().numpy(), want)
