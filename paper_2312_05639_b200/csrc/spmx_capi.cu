@@ -10,6 +10,7 @@
 
 #include <atomic>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <exception>
 #include <new>
@@ -59,11 +60,22 @@ int guarded(F&& f) {
 }
 
 constexpr uint32_t kMagicCtx = 0x58435443, kMagicCsr = 0x58435352, kMagicPlan = 0x58504c4e;
-constexpr u64 kDefaultChunkItems = 1024;  // merge items (rows + nonzeros) per warp-level chunk
+constexpr u64 kDefaultChunkItems = 256;  // merge items (rows + nonzeros) per warp-level chunk
 #ifndef SPMX_LONG_SEG
 #define SPMX_LONG_SEG 256
 #endif
 constexpr unsigned kDefaultLongSeg = SPMX_LONG_SEG;  // row segments >= this are shared by the warp's groups
+
+// tuning knobs, overridable from the environment for experiments (tools/dev_bench.py)
+inline u64 env_u64(const char* name, u64 dflt) {
+  const char* v = std::getenv(name);
+  return (v && *v) ? (u64)std::strtoull(v, nullptr, 10) : dflt;
+}
+inline u64 chunk_items() { return std::max<u64>(64, env_u64("SPMX_CHUNK_ITEMS", kDefaultChunkItems)); }
+inline unsigned long_seg() { return (unsigned)env_u64("SPMX_LONG_SEG", kDefaultLongSeg); }
+// interior chunk boundaries never cut a row shorter than this
+inline u64 snap_len() { return env_u64("SPMX_SNAP_LEN", 128); }
+inline u64 default_parts_per_sm() { return env_u64("SPMX_PARTS_PER_SM", 8); }
 
 inline unsigned blocks_for(u64 n, unsigned threads = 256) {
   return (unsigned)((n + threads - 1) / threads);
@@ -208,11 +220,11 @@ void launch_one(const spmx_plan* p, const spmx_dev::SpmmArgs& args, cudaStream_t
     spmx_dev::spmm_dynamic_kernel<D_CT, G, VEC, NT, RAGGED>
         <<<grid, spmx_dev::kWarpsPerCta * 32, 0, st>>>(args);
   } else {
-    const unsigned grid =
-        (unsigned)((args.n_chunks + spmx_dev::kWarpsPerCta - 1) / spmx_dev::kWarpsPerCta);
+    constexpr int kChunksPerCta = spmx_dev::kWarpsPerCta * (32 / G);  // one chunk per group
+    const unsigned grid = (unsigned)((args.n_chunks + kChunksPerCta - 1) / kChunksPerCta);
     if (grid == 0) return;
 #ifndef SPMX_CARVEOUT
-#define SPMX_CARVEOUT 25  // % of the unified L1/shared array given to shared memory
+#define SPMX_CARVEOUT 30  // % of the unified L1/shared array given to shared memory
 #endif
     // In-flight X-row gathers are held in L1 lines: the kernel needs only a few KB of shared
     // memory, so keep the carve-out small (the driver's default picked 135 KB, leaving the
@@ -288,7 +300,7 @@ void run_kernels(spmx_ctx* ctx, const spmx_plan* p, const spmx_csr* a, const flo
   args.m = (u64)a->m;
   args.ldx = (int)d;
   const bool exact = (p->flags & SPMX_EXACT_ORDER) != 0;
-  args.long_seg = (exact || (p->flags & SPMX_NO_COOP)) ? 0u : kDefaultLongSeg;
+  args.long_seg = (exact || (p->flags & SPMX_NO_COOP)) ? 0u : long_seg();
   args.counter = p->counter;
   args.batch = p->batch;
 
@@ -317,7 +329,7 @@ void run_kernels(spmx_ctx* ctx, const spmx_plan* p, const spmx_csr* a, const flo
         launch_generic<1>(p, args, g, nt, ctx->stream, ctx->sm_count);
     }
     if (p->may_carry && p->n_chunks > 1) {
-      spmx_dev::carry_fixup_kernel<<<(unsigned)(p->n_chunks - 1), 128, 0, ctx->stream>>>(
+      spmx_dev::carry_fixup_kernel<<<blocks_for((p->n_chunks - 1) * (32 / spmx_dev::kFixupPerWarp), 256), 256, 0, ctx->stream>>>(
           a->row_ptr, p->chunk_row, p->chunk_nnz, p->n_chunks, (u64)a->m, p->carry, d_y, (int)d,
           (int)c0, dw);
       post_launch();
@@ -348,7 +360,10 @@ spmx_plan* plan_build(spmx_ctx* ctx, const spmx_csr* a, int strategy, unsigned p
   const u64 m = (u64)a->m, nnz = (u64)a->nnz;
   const bool exact = (flags & SPMX_EXACT_ORDER) != 0;
   if (parts == 0) {
-    const u64 want = (m + nnz + kDefaultChunkItems - 1) / kDefaultChunkItems;
+    // strategy-level ranges T: a few per SM (the device refines them into chunks); exact-order
+    // mode has no refinement, so there T is the work-list size itself
+    const u64 fine = (m + nnz + chunk_items() - 1) / chunk_items();
+    const u64 want = exact ? fine : std::min<u64>(fine, (u64)ctx->sm_count * default_parts_per_sm());
     parts = (unsigned)std::min<u64>(std::max<u64>(want, 1), 1u << 30);
   }
   spmx_plan* p = new spmx_plan;
@@ -382,18 +397,21 @@ spmx_plan* plan_build(spmx_ctx* ctx, const spmx_csr* a, int strategy, unsigned p
           a->row_ptr, d_bnd, (u64)parts + 1, d_diag);
     }
     post_launch();
-    // 3. work list: exact -> one chunk per range; otherwise ranges heavier than the chunk budget
-    //    are cut along the merge path
-    u64* d_cdiag = nullptr;
+    // 3. work list: exact -> one chunk per range, boundaries on rows; otherwise ranges heavier
+    //    than the chunk budget are cut along the merge path (interior cuts snapped to the start
+    //    of short rows)
     if (exact) {
       p->n_chunks = parts;
-      d_cdiag = d_diag;
-      d_diag = nullptr;
+      p->chunk_row = dev_alloc<u64>((size_t)p->n_chunks + 1);
+      p->chunk_nnz = dev_alloc<u64>((size_t)p->n_chunks + 1);
+      spmx_dev::merge_search_kernel<<<blocks_for(p->n_chunks + 1), 256, 0, ctx->stream>>>(
+          a->row_ptr, m, nnz, d_diag, p->n_chunks + 1, p->chunk_row, p->chunk_nnz);
+      post_launch();
     } else {
       u64* d_cnt = dev_alloc<u64>(parts);
       u64* d_off = dev_alloc<u64>((size_t)parts + 1);
       spmx_dev::count_chunks_kernel<<<blocks_for(parts), 256, 0, ctx->stream>>>(
-          d_diag, parts, kDefaultChunkItems, d_cnt);
+          d_diag, parts, chunk_items(), d_cnt);
       post_launch();
       spmx_dev::exclusive_scan_kernel<<<1, 1024, 0, ctx->stream>>>(d_cnt, parts, d_off);
       post_launch();
@@ -402,23 +420,18 @@ spmx_plan* plan_build(spmx_ctx* ctx, const spmx_csr* a, int strategy, unsigned p
                                  ctx->stream));
       CUDA_CHECK(cudaStreamSynchronize(ctx->stream));
       p->n_chunks = total;
-      d_cdiag = dev_alloc<u64>((size_t)total + 1);
-      spmx_dev::chunk_diagonals_kernel<<<blocks_for(total + 1), 256, 0, ctx->stream>>>(
-          d_diag, d_off, parts, total, d_cdiag);
+      p->chunk_row = dev_alloc<u64>((size_t)total + 1);
+      p->chunk_nnz = dev_alloc<u64>((size_t)total + 1);
+      spmx_dev::chunk_coords_kernel<<<blocks_for(total + 1), 256, 0, ctx->stream>>>(
+          a->row_ptr, m, nnz, d_diag, d_off, parts, total, snap_len(), p->chunk_row, p->chunk_nnz);
       post_launch();
       CUDA_CHECK(cudaStreamSynchronize(ctx->stream));
       CUDA_CHECK(cudaFree(d_cnt));
       CUDA_CHECK(cudaFree(d_off));
       p->may_carry = true;
     }
-    p->chunk_row = dev_alloc<u64>((size_t)p->n_chunks + 1);
-    p->chunk_nnz = dev_alloc<u64>((size_t)p->n_chunks + 1);
-    spmx_dev::merge_search_kernel<<<blocks_for(p->n_chunks + 1), 256, 0, ctx->stream>>>(
-        a->row_ptr, m, nnz, d_cdiag, p->n_chunks + 1, p->chunk_row, p->chunk_nnz);
-    post_launch();
     CUDA_CHECK(cudaStreamSynchronize(ctx->stream));
-    CUDA_CHECK(cudaFree(d_cdiag));
-    if (d_diag) CUDA_CHECK(cudaFree(d_diag));
+    CUDA_CHECK(cudaFree(d_diag));
     CUDA_CHECK(cudaFree(d_bnd));
     return p;
   } catch (...) {

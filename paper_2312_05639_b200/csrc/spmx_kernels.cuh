@@ -65,6 +65,10 @@ __device__ __forceinline__ VecT<VEC> ld_x(const float* p) {
   return r;
 }
 
+__device__ __forceinline__ void prefetch_l2(const void* p) {
+  asm volatile("prefetch.global.L2 [%0];" ::"l"(p));
+}
+
 template <int VEC>
 __device__ __forceinline__ void st_y(float* p, const float* a) {
   if constexpr (VEC == 4) {
@@ -114,67 +118,79 @@ __device__ __forceinline__ void zero_acc(float (&acc)[NT][VEC]) {
     for (int v = 0; v < VEC; ++v) acc[t][v] = 0.0f;
 }
 
-constexpr int kWindowRows = 128;  // rows whose bounds a warp stages at a time
-
 #ifndef SPMX_U
 #define SPMX_U 16  // LDG.128 gathers in flight per lane (measured best with 2 CTAs/SM)
 #endif
+#ifndef SPMX_MIN_CTAS
+#define SPMX_MIN_CTAS 2
+#endif
 
-// Per-warp shared memory.
+// Rows whose bounds one group stages at a time (shared memory: 6 bytes per row and group).
 template <int G>
-struct WarpScratch {
-  u32 row_idx[kWindowRows];  // k-th non-empty row of the window (window-local index)
-  u32 row_end[kWindowRows];  // its end, as an offset from the piece's first nonzero
+struct Window {
+  static constexpr int NGW = 32 / G;
+  static constexpr int kRows = (512 / NGW) > 128 ? 128 : (512 / NGW);
 };
 
-// Processes the piece of the merge path between (r0, j0) and (r1, j1) with one warp.
-// Rows [r0, r1) end inside the piece and are stored to Y; when the piece ends in the
-// middle of row r1 (has_carry) the partial sum of its nonzeros [.., j1) goes to
-// carry_row. A row whose head lies in an earlier piece is stored like any other row;
-// carry_fixup_kernel adds the earlier partials afterwards.
+// Per-warp shared memory: one region per group.
+template <int G>
+struct WarpScratch {
+  u32 row_end[Window<G>::NGW][Window<G>::kRows];             // end of the k-th non-empty row,
+                                                             // offset from the piece's first nnz
+  unsigned short row_idx[Window<G>::NGW][Window<G>::kRows];  // its window-local row index
+};
+
+// One piece of the merge path per GROUP of G lanes: the nonzeros and row ends between the
+// coordinates (r0, j0) and (r1, j1). Rows [r0, r1) end inside the piece and are stored to Y;
+// when the piece ends in the middle of row r1 (has_carry) the partial sum of that row's
+// nonzeros [.., j1) goes to carry_row. A row whose head lies in an earlier piece is stored
+// like any other row; carry_fixup_kernel adds the earlier partials afterwards, in CSR order.
+// The 32/G groups of a warp run the same instruction stream on different pieces (all loop
+// trip counts are made warp-uniform; pieces hold the same number of merge items, so the
+// groups finish together).
 //
-// Load phase and reduce phase are decoupled. Rows are staged kWindowRows at a time
-// (bounds clipped to the piece, empty rows zeroed on the spot, the others compacted
-// into shared memory). The staged rows are then consumed as a sequence of segments:
-//   * a run of ordinary rows: its nonzero range is cut into 32/G contiguous sub-streams,
-//     one per group of G lanes, cuts moved back to row starts, so every row is summed by
-//     one group as one fmaf chain in CSR order (bitwise equal to the reference);
-//   * one long row (>= long_seg nonzeros, or the row the piece ends in): cut evenly
-//     between the groups, partial sums added in CSR order of the cuts by shuffles.
-// A group walks its sub-stream through a rotating U-deep register pipeline: the X-row
-// gather for nonzero q+U is issued as soon as nonzero q has been consumed, whatever the
-// row structure. Column indices, values and the "row ends here" marks are produced a batch
-// of G positions ahead (coalesced streaming loads; marks scattered through shared memory)
-// and broadcast by shuffles, so the reduce step is: fma; if marked, store the row, zero.
-// The piece must span fewer than 2^32 nonzeros (the plan guarantees it).
+// Load phase and reduce phase are decoupled. A group stages the bounds of its next rows
+// (clipped to the piece) in shared memory — empty rows are zeroed on the spot, the others
+// compacted — and then streams the nonzeros of those rows through a rotating U-deep register
+// pipeline: the X-row gather for nonzero q+U is issued as soon as nonzero q has been
+// consumed, whatever the row structure. Column indices and values are fetched a batch of G
+// positions ahead (coalesced streaming loads) and broadcast inside the group by shuffles.
+// The reduce step is acc = fmaf(v, x, acc) plus a countdown to the row end; at a row end the
+// row is stored and the accumulators are zeroed. Every row that lies wholly inside a piece
+// is therefore ONE fmaf chain in CSR order: bitwise equal to the reference.
+// A piece must span fewer than 2^32 nonzeros (the plan guarantees it).
 template <int D_CT, int G, int VEC, int NT, bool RAGGED>
-__device__ __forceinline__ void process_piece(const SpmmArgs& a, u64 r0, u64 j0, u64 r1, u64 j1,
-                                              bool has_carry, float* carry_row, int lane,
-                                              WarpScratch<G>& sm) {
+__device__ __forceinline__ void process_piece(const SpmmArgs& a, bool active, u64 r0, u64 j0,
+                                              u64 r1, u64 j1, bool has_carry, float* carry_row,
+                                              int lane, WarpScratch<G>& sm) {
   constexpr int NGW = 32 / G;
+  constexpr int W = Window<G>::kRows;
   constexpr int UMAX = (SPMX_U / NT) > 0 ? (SPMX_U / NT) : 1;
   constexpr int U = UMAX < G ? UMAX : G;  // gathers in flight per lane; divides G
   const int g = lane / G, lg = lane % G;
   const int ldx = D_CT ? D_CT : a.ldx;
-  const u64 row_lim = r1 + (has_carry ? 1 : 0);
+  const u64 row_lim = active ? r1 + (has_carry ? 1 : 0) : r0;
   const u32* __restrict__ colp = a.col + j0;
   const float* __restrict__ valp = a.vals + j0;
   const float* __restrict__ xbase = a.x + a.c0 + lg * VEC;
-  const u32 span = (u32)(j1 - j0);
-  const u32 long_seg = (NGW > 1 && a.long_seg != 0) ? a.long_seg : 0xffffffffu;
-  const unsigned lt_mask = (1u << lane) - 1u;
+  const u32 span = active ? (u32)(j1 - j0) : 0u;
+  const unsigned grp_mask = (G == 32) ? kFullMask : (((1u << G) - 1u) << (g * G));
+  const unsigned lt_mask = grp_mask & ((1u << lane) - 1u);
+  u32* __restrict__ s_end = sm.row_end[g];
+  unsigned short* __restrict__ s_idx = sm.row_idx[g];
   float acc[NT][VEC];
 
   u32 ws = 0;  // nonzero offset where the current window starts
-  for (u64 wbase = r0; wbase < row_lim; wbase += kWindowRows) {
-    const int nw = (int)min((u64)kWindowRows, row_lim - wbase);
+  for (u64 wbase = r0; __any_sync(kFullMask, wbase < row_lim); wbase += W) {
+    const int nw = wbase < row_lim ? (int)min((u64)W, row_lim - wbase) : 0;
     // ---- stage the window: clipped row ends, compacted over non-empty rows ----------------
     int count = 0;
     __syncwarp();
     zero_acc(acc);
+    const int nw_max = __reduce_max_sync(kFullMask, nw);
 #pragma unroll 1
-    for (int q0 = 0; q0 < nw; q0 += 32) {
-      const int li = q0 + lane;
+    for (int q0 = 0; q0 < nw_max; q0 += G) {
+      const int li = q0 + lg;
       u32 s = 0, e = 0;
       const bool valid = li < nw;
       if (valid) {
@@ -182,24 +198,19 @@ __device__ __forceinline__ void process_piece(const SpmmArgs& a, u64 r0, u64 j0,
         s = lo > j0 ? (u32)min(lo - j0, (u64)span) : 0u;
         e = hi > j0 ? (u32)min(hi - j0, (u64)span) : 0u;
       }
-      const unsigned ne = __ballot_sync(kFullMask, valid && e != s);
+      const unsigned ne = __ballot_sync(kFullMask, valid && e != s) & grp_mask;
       if (valid && e != s) {
         const int pos = count + __popc(ne & lt_mask);
-        sm.row_idx[pos] = (u32)li;
-        sm.row_end[pos] = e;
+        s_idx[pos] = (unsigned short)li;
+        s_end[pos] = e;
       }
       count += __popc(ne);
-      // empty rows: zeros, NGW rows per store instruction
-      unsigned em = __ballot_sync(kFullMask, valid && e == s);
-      while (em) {
-        int src = -1;
-#pragma unroll
-        for (int q = 0; q < NGW; ++q) {
-          const int bit = em ? __ffs(em) - 1 : -1;
-          if (q == g) src = bit;
-          if (em) em &= em - 1;
-        }
-        if (src >= 0) {
+      // empty rows: the whole group writes one row of zeros at a time
+      unsigned em = __ballot_sync(kFullMask, valid && e == s) & grp_mask;
+      while (__any_sync(kFullMask, em != 0)) {
+        if (em) {
+          const int src = (__ffs(em) - 1) - g * G;
+          em &= em - 1;
           const u64 rr = wbase + q0 + src;
           float* dst = (rr < r1) ? a.y + (size_t)rr * (size_t)ldx : carry_row;
           store_row<G, VEC, NT, RAGGED>(a, dst, lg, acc);
@@ -207,233 +218,195 @@ __device__ __forceinline__ void process_piece(const SpmmArgs& a, u64 r0, u64 j0,
       }
     }
     __syncwarp();
-    if (count == 0) continue;
-    const u32 we = sm.row_end[count - 1];
-    float* __restrict__ ybase = a.y + (size_t)wbase * (size_t)ldx;
+    const u32 we = count > 0 ? s_end[count - 1] : ws;
+    const u32 L = we - ws;  // nonzeros of this window in this group's piece
+    const u32 Lmax = __reduce_max_sync(kFullMask, L);
+    if (Lmax == 0) continue;  // warp-uniform
+    const u32 p0 = ws;
+    int k = 0;  // current row = k-th non-empty row of the window
+    u32 left = (L > 0) ? s_end[0] - p0 : 0x7fffffffu;  // nonzeros left in the current row
 
-    // ---- which staged rows are "long" (shared by all groups) ------------------------------
-    unsigned longm[kWindowRows / 32];
+    // ---- walk the window's nonzeros ---------------------------------------------------------
+    u32 c0 = 0, c1 = 0;
+    float v0 = 0.0f, v1 = 0.0f;
+    if ((u32)lg < L) { c0 = __ldcs(colp + p0 + lg); v0 = __ldcs(valp + p0 + lg); }
+    if ((u32)(G + lg) < L) { c1 = __ldcs(colp + p0 + G + lg); v1 = __ldcs(valp + p0 + G + lg); }
+    VecT<VEC> xv[U][NT];
 #pragma unroll
-    for (int q = 0; q < kWindowRows / 32; ++q) {
-      const int kk = q * 32 + lane;
-      bool is_long = false;
-      if (kk < count) {
-        const u32 rs = kk > 0 ? sm.row_end[kk - 1] : ws;
-        is_long = (sm.row_end[kk] - rs >= long_seg) ||
-                  (has_carry && wbase + sm.row_idx[kk] == r1);
+    for (int u = 0; u < U; ++u) {
+      const u32 kq = __shfl_sync(kFullMask, c0, u, G);
+      if ((u32)u < L) {
+        const float* xr = xbase + (size_t)kq * (size_t)ldx;
+#pragma unroll
+        for (int t = 0; t < NT; ++t)
+          if (!RAGGED || (t * G + lg) * VEC < a.dw) xv[u][t] = ld_x<VEC>(xr + t * G * VEC);
       }
-      longm[q] = __ballot_sync(kFullMask, is_long);
     }
-
-    // ---- consume the window as segments: [run of ordinary rows] [long row] ... --------------
-    int seg_k = 0;
-    for (;;) {
-      // next long row at or after seg_k
-      int kl = count;
+#ifndef SPMX_PF
+#define SPMX_PF 96  // positions ahead at which the col/val stream is pulled into L2
+#endif
+    if (SPMX_PF > 0) {  // the first lines of the stream
 #pragma unroll
-      for (int q = kWindowRows / 32 - 1; q >= 0; --q) {
-        unsigned mq = longm[q];
-        if (seg_k > q * 32) mq = (seg_k >= (q + 1) * 32) ? 0u : (mq & ~((1u << (seg_k - q * 32)) - 1u));
-        if (mq) kl = q * 32 + __ffs(mq) - 1;
-      }
-      bool is_long_seg;
-      int ka, kb;  // rows [ka, kb) of this segment
-      if (seg_k < kl) { is_long_seg = false; ka = seg_k; kb = kl; }
-      else if (kl < count) { is_long_seg = true; ka = kl; kb = kl + 1; }
-      else break;
-      seg_k = kb;
-
-      const u32 sa = ka > 0 ? sm.row_end[ka - 1] : ws;
-      const u32 sb = sm.row_end[kb - 1];
-      // ---- cut [sa, sb) into NGW sub-streams ------------------------------------------------
-      u32 p0 = sa, pe = sb;
-      int k0 = ka, k1 = kb;  // rows of this group (ordinary segment)
-      if constexpr (NGW > 1) {
-        const u32 len = sb - sa;
-        const u32 q = (len + NGW - 1) / NGW;
-        u32 cut[2];
-        int kcut[2];
-#pragma unroll
-        for (int side = 0; side < 2; ++side) {
-          const int gg = g + side;
-          u32 bnd = sa + min((u32)gg * q, len);
-          int kk = gg >= NGW ? kb : ka;
-          if (!is_long_seg && gg > 0 && gg < NGW) {
-            int lo = ka, hi = kb;  // first row with end > bnd
-            while (lo < hi) {
-              const int mid_i = (lo + hi) >> 1;
-              if (sm.row_end[mid_i] > bnd) hi = mid_i; else lo = mid_i + 1;
-            }
-            kk = lo;
-            bnd = kk < kb ? (kk > ka ? sm.row_end[kk - 1] : sa) : sb;  // back to the row start
-          }
-          cut[side] = bnd;
-          kcut[side] = kk;
-        }
-        p0 = cut[0];
-        pe = cut[1];
-        k0 = kcut[0];
-        k1 = kcut[1];
-      }
-      const u32 L = pe - p0;  // this group's sub-stream length
-      const u32 Lmax = __reduce_max_sync(kFullMask, L);
-      int k = k0;  // current row of this group
-      // nonzeros left in the current row; a long row's end is handled after the loop
-      u32 left = (!is_long_seg && L > 0) ? sm.row_end[k] - p0 : 0x7fffffffu;
-
-      u32 c0 = 0, c1 = 0;
-      float v0 = 0.0f, v1 = 0.0f;
-      if ((u32)lg < L) { c0 = __ldcs(colp + p0 + lg); v0 = __ldcs(valp + p0 + lg); }
-      if ((u32)(G + lg) < L) { c1 = __ldcs(colp + p0 + G + lg); v1 = __ldcs(valp + p0 + G + lg); }
-      VecT<VEC> xv[U][NT];
-#pragma unroll
-      for (int u = 0; u < U; ++u) {
-        const u32 kq = __shfl_sync(kFullMask, c0, u, G);
-        if ((u32)u < L) {
-          const float* xr = xbase + (size_t)kq * (size_t)ldx;
-#pragma unroll
-          for (int t = 0; t < NT; ++t)
-            if (!RAGGED || (t * G + lg) * VEC < a.dw) xv[u][t] = ld_x<VEC>(xr + t * G * VEC);
-        }
-      }
+      for (int q = 2 * G; q < SPMX_PF; q += G)
+        if ((u32)(q + lg) < L) { prefetch_l2(colp + p0 + q + lg); prefetch_l2(valp + p0 + q + lg); }
+    }
 #pragma unroll 1
-      for (u32 nb = 0; nb < Lmax; nb += G) {
-        u32 c2 = 0;
-        float v2 = 0.0f;
-        if (nb + 2 * G + lg < L) {
-          c2 = __ldcs(colp + p0 + nb + 2 * G + lg);
-          v2 = __ldcs(valp + p0 + nb + 2 * G + lg);
-        }
-#pragma unroll
-        for (int t = 0; t < G; ++t) {
-          const int u = t % U;
-          const float vq = __shfl_sync(kFullMask, v0, t, G);
-          const u32 kq = (t + U < G) ? __shfl_sync(kFullMask, c0, t + U, G)
-                                     : __shfl_sync(kFullMask, c1, t + U - G, G);
-          if (nb + t < L) {
-#pragma unroll
-            for (int tt = 0; tt < NT; ++tt)
-              if (!RAGGED || (tt * G + lg) * VEC < a.dw) {
-#pragma unroll
-                for (int e = 0; e < VEC; ++e)
-                  acc[tt][e] = __fmaf_rn(vq, xv[u][tt].v[e], acc[tt][e]);
-              }
-          }
-#ifdef SPMX_EXP_NOROWEND
-          if (false) {
-#else
-          if (--left == 0) {  // row k ends here: store it, start the next one
-#endif
-#ifndef SPMX_EXP_NOSTORE
-            store_row<G, VEC, NT, RAGGED>(a, ybase + (size_t)sm.row_idx[k] * (size_t)ldx, lg, acc);
-#endif
-            zero_acc(acc);
-            ++k;
-            left = (k < k1) ? sm.row_end[k] - sm.row_end[k - 1] : 0x7fffffffu;
-          }
-          if (nb + t + U < L) {
-            const float* xr = xbase + (size_t)kq * (size_t)ldx;
-#pragma unroll
-            for (int tt = 0; tt < NT; ++tt)
-              if (!RAGGED || (tt * G + lg) * VEC < a.dw) xv[u][tt] = ld_x<VEC>(xr + tt * G * VEC);
-          }
-        }
-        c0 = c1; v0 = v1;
-        c1 = c2; v1 = v2;
+    for (u32 nb = 0; nb < Lmax; nb += G) {
+      u32 c2 = 0;
+      float v2 = 0.0f;
+      if (nb + 2 * G + lg < L) {
+        c2 = __ldcs(colp + p0 + nb + 2 * G + lg);
+        v2 = __ldcs(valp + p0 + nb + 2 * G + lg);
       }
-
-      if (is_long_seg) {  // add the groups' partial sums in CSR order of the cuts, store once
-        if constexpr (NGW > 1) {
-          float tot[NT][VEC];
+      if (SPMX_PF > 0 && nb + SPMX_PF + lg < L) {  // DRAM latency is paid here, off the critical path
+        prefetch_l2(colp + p0 + nb + SPMX_PF + lg);
+        prefetch_l2(valp + p0 + nb + SPMX_PF + lg);
+      }
 #pragma unroll
-          for (int t = 0; t < NT; ++t)
+      for (int t = 0; t < G; ++t) {
+        const int u = t % U;
+        const float vq = __shfl_sync(kFullMask, v0, t, G);
+        const u32 kq = (t + U < G) ? __shfl_sync(kFullMask, c0, t + U, G)
+                                   : __shfl_sync(kFullMask, c1, t + U - G, G);
+        if (nb + t < L) {
 #pragma unroll
-            for (int e = 0; e < VEC; ++e) {
-              float sacc = __shfl_sync(kFullMask, acc[t][e], lg);
+          for (int tt = 0; tt < NT; ++tt)
+            if (!RAGGED || (tt * G + lg) * VEC < a.dw) {
 #pragma unroll
-              for (int gg = 1; gg < NGW; ++gg) sacc += __shfl_sync(kFullMask, acc[t][e], gg * G + lg);
-              tot[t][e] = sacc;
+              for (int e = 0; e < VEC; ++e)
+                acc[tt][e] = __fmaf_rn(vq, xv[u][tt].v[e], acc[tt][e]);
             }
-#pragma unroll
-          for (int t = 0; t < NT; ++t)
-#pragma unroll
-            for (int e = 0; e < VEC; ++e) acc[t][e] = tot[t][e];
         }
-        if (g == 0) {
-          const u64 rr = wbase + sm.row_idx[ka];
+        if (--left == 0) {  // row k ends here: store it, start the next one
+          const u64 rr = wbase + s_idx[k];
           float* dst = (rr < r1) ? a.y + (size_t)rr * (size_t)ldx : carry_row;
           store_row<G, VEC, NT, RAGGED>(a, dst, lg, acc);
+          zero_acc(acc);
+          ++k;
+          left = (k < count) ? s_end[k] - s_end[k - 1] : 0x7fffffffu;
         }
-        zero_acc(acc);
+        if (nb + t + U < L) {
+          const float* xr = xbase + (size_t)kq * (size_t)ldx;
+#pragma unroll
+          for (int tt = 0; tt < NT; ++tt)
+            if (!RAGGED || (tt * G + lg) * VEC < a.dw) xv[u][tt] = ld_x<VEC>(xr + tt * G * VEC);
+        }
       }
+      c0 = c1; v0 = v1;
+      c1 = c2; v1 = v2;
     }
     ws = we;
   }
 }
 
-#ifndef SPMX_MIN_CTAS
-#define SPMX_MIN_CTAS 2
-#endif
-
-// Static work list: warp w of the grid owns chunk w.
+// Static work list: group s of the grid (G lanes) owns chunk s.
 template <int D_CT, int G, int VEC, int NT, bool RAGGED>
 __global__ void __launch_bounds__(kWarpsPerCta * 32, (NT <= 2 ? SPMX_MIN_CTAS : 1))
 spmm_chunk_kernel(const SpmmArgs a) {
+  constexpr int NGW = 32 / G;
   __shared__ WarpScratch<G> scratch[kWarpsPerCta];
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
-  const u64 chunk = (u64)blockIdx.x * kWarpsPerCta + w;
-  if (chunk >= a.n_chunks) return;
-  const u64 r0 = a.chunk_row[chunk], j0 = a.chunk_nnz[chunk];
-  const u64 r1 = a.chunk_row[chunk + 1], j1 = a.chunk_nnz[chunk + 1];
-  const bool has_carry = (r1 < a.m) && (j1 > (u64)__ldg(a.row_ptr + r1));
+  const u64 warp = (u64)blockIdx.x * kWarpsPerCta + w;
+  if (warp * NGW >= a.n_chunks) return;  // whole warp idle
+  const u64 chunk = warp * NGW + lane / G;
+  const bool active = chunk < a.n_chunks;
+  u64 r0 = 0, j0 = 0, r1 = 0, j1 = 0;
+  bool has_carry = false;
+  if (active) {
+    r0 = a.chunk_row[chunk]; j0 = a.chunk_nnz[chunk];
+    r1 = a.chunk_row[chunk + 1]; j1 = a.chunk_nnz[chunk + 1];
+    has_carry = (r1 < a.m) && (j1 > (u64)__ldg(a.row_ptr + r1));
+  }
   const int ldx = D_CT ? D_CT : a.ldx;
-  float* carry_row = a.carry_out ? a.carry_out + (size_t)chunk * (size_t)ldx : nullptr;
-  process_piece<D_CT, G, VEC, NT, RAGGED>(a, r0, j0, r1, j1, has_carry, carry_row, lane,
+  float* carry_row = (a.carry_out && active) ? a.carry_out + (size_t)chunk * (size_t)ldx : nullptr;
+  process_piece<D_CT, G, VEC, NT, RAGGED>(a, active, r0, j0, r1, j1, has_carry, carry_row, lane,
                                           scratch[w]);
 }
 
 // Dynamic row dispatch (row-split only): persistent warps claim `batch` rows at a time
 // from a device counter — next_batch(), src/partition.cpp:29-33; the JIT'd `lock xadd`
 // driver, src/jit.cpp:106-121. One claim per warp keeps the claimed ranges disjoint and
-// covering [0, m) exactly as the reference's dispatcher does.
+// covering [0, m) exactly as the reference's dispatcher does; the claimed rows are dealt
+// to the warp's groups in equal contiguous shares (rows are never split).
 template <int D_CT, int G, int VEC, int NT, bool RAGGED>
 __global__ void __launch_bounds__(kWarpsPerCta * 32, (NT <= 2 ? SPMX_MIN_CTAS : 1))
 spmm_dynamic_kernel(const SpmmArgs a) {
+  constexpr int NGW = 32 / G;
   __shared__ WarpScratch<G> scratch[kWarpsPerCta];
-  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5, g = lane / G;
   for (;;) {
     u64 v = 0;
     if (lane == 0) v = atomicAdd(a.counter, a.batch);
     v = __shfl_sync(kFullMask, v, 0);
     if (v >= a.m) return;
     const u64 hi = min(v + a.batch, a.m);
-    const u64 j0 = __ldg(a.row_ptr + v), j1 = __ldg(a.row_ptr + hi);
-    process_piece<D_CT, G, VEC, NT, RAGGED>(a, v, j0, hi, j1, false, nullptr, lane, scratch[w]);
+    const u64 share = (hi - v + NGW - 1) / NGW;
+    const u64 b = min(v + (u64)g * share, hi), e = min(b + share, hi);
+    const u64 j0 = __ldg(a.row_ptr + b), j1 = __ldg(a.row_ptr + e);
+    process_piece<D_CT, G, VEC, NT, RAGGED>(a, b < e, b, j0, e, j1, false, nullptr, lane,
+                                            scratch[w]);
   }
 }
 
 // Adds the partial sums of rows cut by chunk boundaries, in CSR order of the pieces:
 // Y[r] = carry_out[u0] + ... + carry_out[t] + (tail already stored in Y[r]).
-// One CTA per chunk; only the last chunk of each chain of carries does work.
-__global__ void carry_fixup_kernel(const u64* __restrict__ row_ptr,
-                                   const u64* __restrict__ chunk_row,
-                                   const u64* __restrict__ chunk_nnz, u64 n_chunks, u64 m,
-                                   const float* __restrict__ carry_out, float* __restrict__ y,
-                                   int ldx, int c0, int dw) {
-  const u64 t = blockIdx.x;
-  if (t + 1 >= n_chunks) return;  // the last chunk ends at (m, nnz): no carry
-  const u64 r = chunk_row[t + 1];
-  if (r >= m) return;
-  const u64 rp = row_ptr[r];
-  if (!(chunk_nnz[t + 1] > rp)) return;     // boundary t+1 is not inside row r
-  if (chunk_row[t + 2] == r) return;        // chunk t+1 carries the same row on: not last
-  u64 u0 = t;
-  while (u0 > 0 && chunk_row[u0] == r && chunk_nnz[u0] > rp) --u0;
-  for (int c = threadIdx.x; c < dw; c += blockDim.x) {
-    float s = carry_out[(size_t)u0 * ldx + c0 + c];
-    for (u64 u = u0 + 1; u <= t; ++u) s += carry_out[(size_t)u * ldx + c0 + c];
-    float* dst = y + (size_t)r * ldx + c0 + c;
-    *dst = s + *dst;
+// A warp inspects kFixupPerWarp consecutive chunk boundaries (one per lane; few per warp, so
+// that many chains are resolved concurrently across warps); for every boundary that closes a
+// chain of carries the whole warp sums that chain, lane c handling columns c, c+32, ... of
+// the slab.
+constexpr int kFixupPerWarp = 8;
+__global__ void __launch_bounds__(256)
+carry_fixup_kernel(const u64* __restrict__ row_ptr, const u64* __restrict__ chunk_row,
+                   const u64* __restrict__ chunk_nnz, u64 n_chunks, u64 m,
+                   const float* __restrict__ carry_out, float* __restrict__ y, int ldx, int c0,
+                   int dw) {
+  const int lane = threadIdx.x & 31;
+  const u64 warp = ((u64)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const u64 t = warp * kFixupPerWarp + lane;  // chunk whose END boundary this lane inspects
+  bool closes = false;
+  u64 r = 0, u0 = 0;
+  if (lane < kFixupPerWarp && t + 1 < n_chunks) {  // the last chunk ends at (m, nnz): no carry
+    r = chunk_row[t + 1];
+    if (r < m) {
+      const u64 rp = __ldg(row_ptr + r);
+      // boundary t+1 lies inside row r, and chunk t+1 does not carry the same row on
+      if (chunk_nnz[t + 1] > rp && chunk_row[t + 2] != r) {
+        closes = true;
+        // the chain starts in the chunk that holds the row's first nonzero: the last chunk u
+        // with chunk_nnz[u] <= rp (binary search instead of walking the chain backwards)
+        u64 lo = 0, hi = t;
+        while (lo < hi) {
+          const u64 mid = lo + (hi - lo + 1) / 2;
+          if (chunk_nnz[mid] <= rp) lo = mid; else hi = mid - 1;
+        }
+        u0 = lo;
+      }
+    }
+  }
+  unsigned todo = __ballot_sync(kFullMask, closes);
+  while (todo) {
+    const int src = __ffs(todo) - 1;
+    todo &= todo - 1;
+    const u64 rr = __shfl_sync(kFullMask, r, src);
+    const u64 first = __shfl_sync(kFullMask, u0, src);
+    const u64 last = warp * kFixupPerWarp + src;
+    for (int c = lane; c < dw; c += 32) {
+      const float* __restrict__ src_c = carry_out + c0 + c;
+      float* dst = y + (size_t)rr * ldx + c0 + c;
+      const float tail = *dst;
+      float s = src_c[(size_t)first * ldx];
+      u64 u = first + 1;
+      // the adds stay in CSR order; the loads of a batch are independent and overlap
+      for (; u + 16 <= last + 1; u += 16) {
+        float part[16];
+#pragma unroll
+        for (int q = 0; q < 16; ++q) part[q] = __ldcs(src_c + (size_t)(u + q) * ldx);
+#pragma unroll
+        for (int q = 0; q < 16; ++q) s += part[q];
+      }
+      for (; u <= last; ++u) s += src_c[(size_t)u * ldx];
+      *dst = s + tail;
+    }
   }
 }
 

@@ -148,22 +148,43 @@ __global__ void exclusive_scan_kernel(const u64* __restrict__ cnt, u64 n, u64* _
   }
 }
 
-// Chunk c belongs to range t = upper_bound(off, c) - 1 and is its s-th piece; its
-// starting diagonal is diag[t] + floor(s * items / cnt) (even split of the range).
-__global__ void chunk_diagonals_kernel(const u64* __restrict__ diag, const u64* __restrict__ off,
-                                       u64 parts, u64 n_chunks, u64* __restrict__ cdiag) {
+// Work-list coordinates. Chunk c belongs to range t = upper_bound(off, c) - 1 and is its
+// s-th piece; its starting diagonal is diag[t] + floor(s * items / cnt) (even split of the
+// range), located on the merge path with the reference's own search. s == 0 is the
+// strategy's boundary and is kept exactly. An interior boundary that falls inside a row
+// shorter than snap_len is moved back to the start of that row: short rows are then never
+// cut (they stay one fmaf chain, bitwise equal to the reference, and need no carry), only
+// long rows are shared between chunks.
+__global__ void chunk_coords_kernel(const u64* __restrict__ row_ptr, u64 m, u64 nnz,
+                                    const u64* __restrict__ diag, const u64* __restrict__ off,
+                                    u64 parts, u64 n_chunks, u64 snap_len,
+                                    u64* __restrict__ out_row, u64* __restrict__ out_nnz) {
   const u64 c = (u64)blockIdx.x * blockDim.x + threadIdx.x;
   if (c > n_chunks) return;
-  if (c == n_chunks) { cdiag[c] = diag[parts]; return; }
-  u64 lo = 0, hi = parts;  // last t with off[t] <= c
-  while (lo + 1 < hi) {
-    const u64 mid = lo + (hi - lo) / 2;
-    if (off[mid] <= c) lo = mid; else hi = mid;
+  u64 k;
+  bool interior = false;
+  if (c == n_chunks) {
+    k = diag[parts];
+  } else {
+    u64 lo = 0, hi = parts;  // last t with off[t] <= c
+    while (lo + 1 < hi) {
+      const u64 mid = lo + (hi - lo) / 2;
+      if (off[mid] <= c) lo = mid; else hi = mid;
+    }
+    const u64 t = lo, s = c - off[t], cnt = off[t + 1] - off[t];
+    const u64 items = diag[t + 1] - diag[t];
+    // s < cnt <= items/chunk+1: s*items fits u64 for any realistic size
+    k = diag[t] + (s * items) / cnt;
+    interior = s != 0;
   }
-  const u64 t = lo, s = c - off[t], cnt = off[t + 1] - off[t];
-  const u64 items = diag[t + 1] - diag[t];
-  // s < cnt <= items/chunk+1: s*items fits u64 for any realistic size (items < 2^40, cnt < 2^24)
-  cdiag[c] = diag[t] + (s * items) / cnt;
+  u64 i, j;
+  merge_search_dev(row_ptr, m, nnz, k, i, j);
+  if (interior && i < m) {
+    const u64 rs = __ldg(row_ptr + i);
+    if (j > rs && __ldg(row_ptr + i + 1) - rs < snap_len) j = rs;
+  }
+  out_row[c] = i;
+  out_nnz[c] = j;
 }
 
 // validate_csr, src/csr.cpp:18-42, on the device. err receives the largest code seen:
