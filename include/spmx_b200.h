@@ -130,7 +130,9 @@ int spmx_spmm(spmx_ctx* ctx, const spmx_plan* plan, const spmx_csr* a, const flo
               int64_t x_rows, int64_t d, float* d_y, float* elapsed_ms);
 
 /* ---- run_spmm(A, X, cfg) with HOST buffers (executor.hpp:44-45): upload A and X, partition,
- *      multiply, download Y. times_ms[0..5] (optional) = {h2d, plan, kernel, d2h, total, unused}.
+ *      multiply, download Y, pipelined over row blocks (col/vals upload, compute and Y download
+ *      overlap). times_ms[0..5] (optional) = {row_ptr upload + plan, same, X upload wait,
+ *      first block ready -> last Y byte, total wall, number of blocks}.
  *      For repeated calls on the same matrix keep the handles and use spmx_spmm instead. ------ */
 int spmx_spmm_host(spmx_ctx* ctx, int64_t m, int64_t n, int64_t nnz, const uint64_t* row_ptr,
                    const uint32_t* col_indices, const float* vals, const float* x, int64_t x_rows,

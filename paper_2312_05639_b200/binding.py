@@ -264,7 +264,7 @@ class Context:
         self.L.check(self.L.lib.spmx_spmm_host(self.h, m, n, nnz, _ptr(rp), _ptr(col) if col.size else 0,
                                                _ptr(vals) if vals.size else 0, _ptr(x), x_rows, d,
                                                _ptr(y), s, parts, int(dynamic), batch, flags, t))
-        return y, dict(h2d=t[0], plan=t[1], kernel=t[2], d2h=t[3], total=t[4])
+        return y, dict(plan=t[0], x_wait=t[2], stream_blocks=t[3], total=t[4], blocks=t[5])
 
     def spmm_reference(self, a: "DeviceCsr", x, y):
         """spmm_reference (unfused Alg. 1) on the device, for verification."""

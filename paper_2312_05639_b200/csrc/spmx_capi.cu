@@ -9,6 +9,7 @@
 #include <cuda_runtime.h>
 
 #include <atomic>
+#include <chrono>
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
@@ -71,7 +72,12 @@ inline u64 env_u64(const char* name, u64 dflt) {
   const char* v = std::getenv(name);
   return (v && *v) ? (u64)std::strtoull(v, nullptr, 10) : dflt;
 }
-inline u64 chunk_items() { return std::max<u64>(64, env_u64("SPMX_CHUNK_ITEMS", kDefaultChunkItems)); }
+inline u64 chunk_items() { return std::max<u64>(32, env_u64("SPMX_CHUNK_ITEMS", kDefaultChunkItems)); }
+// small inputs: shrink the chunks until there are enough of them to occupy every SM
+inline u64 chunk_items_for(u64 items, int sm_count) {
+  const u64 want_chunks = (u64)sm_count * 64;
+  return std::min<u64>(chunk_items(), std::max<u64>(32, items / want_chunks));
+}
 inline unsigned long_seg() { return (unsigned)env_u64("SPMX_LONG_SEG", kDefaultLongSeg); }
 // interior chunk boundaries never cut a row shorter than this
 inline u64 snap_len() { return env_u64("SPMX_SNAP_LEN", 128); }
@@ -91,6 +97,8 @@ struct spmx_ctx {
   int sm_count = 0;
   cudaEvent_t ev0 = nullptr, ev1 = nullptr;
   int* d_err = nullptr;  // device-side error flag for validation
+  cudaStream_t s_compute = nullptr, s_d2h = nullptr;  // spmx_spmm_host pipeline (lazy)
+  std::vector<cudaEvent_t> pipe_events;                // created once, reused by every call
   // grow-only staging used by spmx_spmm_host
   void* ws[5] = {nullptr, nullptr, nullptr, nullptr, nullptr};
   size_t ws_bytes[5] = {0, 0, 0, 0, 0};
@@ -148,6 +156,19 @@ T* dev_alloc(size_t count) {
   return p;
 }
 
+// Stream-ordered allocations for plans and their temporaries: no device-wide synchronisation
+// (cudaMalloc/cudaFree serialise against transfers in flight), and after the first plan the
+// pool hands the same memory back in microseconds.
+template <typename T>
+T* dev_alloc_async(spmx_ctx* ctx, size_t count) {
+  T* p = nullptr;
+  CUDA_CHECK(cudaMallocAsync(&p, (count ? count : 1) * sizeof(T), ctx->stream));
+  return p;
+}
+void dev_free_async(spmx_ctx* ctx, void* p) {
+  if (p) cudaFreeAsync(p, ctx->stream);
+}
+
 void launched(unsigned n = 1) { g_launches.fetch_add(n, std::memory_order_relaxed); }
 
 void post_launch() {
@@ -189,19 +210,30 @@ void ranges_to_host(spmx_ctx* ctx, const u64* d_bnd, unsigned parts, uint64_t* o
   CUDA_CHECK(cudaFree(d_ranges));
 }
 
+const char* csr_error_text(int err) {
+  static const char* what[] = {"", "", "row_ptr[0] != 0", "row_ptr[m] != nnz",
+                               "row_ptr not nondecreasing", "column index out of range"};
+  return what[err < 0 || err > 5 ? 0 : err];
+}
+
+unsigned validate_grid(spmx_ctx* ctx, u64 work) {
+  return (unsigned)std::min<u64>((u64)ctx->sm_count * 8, std::max<u64>(1, (work + 255) / 256));
+}
+
 void validate_on_device(spmx_ctx* ctx, const spmx_csr* a) {
   CUDA_CHECK(cudaMemsetAsync(ctx->d_err, 0, sizeof(int), ctx->stream));
-  const unsigned nb = (unsigned)std::min<u64>(
-      (u64)ctx->sm_count * 8, std::max<u64>(1, ((u64)a->nnz + (u64)a->m + 255) / 256));
-  spmx_dev::validate_csr_kernel<<<nb, 256, 0, ctx->stream>>>(a->row_ptr, a->col, (u64)a->m,
-                                                             (u64)a->n, (u64)a->nnz, ctx->d_err);
+  spmx_dev::validate_row_ptr_kernel<<<validate_grid(ctx, (u64)a->m), 256, 0, ctx->stream>>>(
+      a->row_ptr, (u64)a->m, (u64)a->nnz, ctx->d_err);
   post_launch();
+  if (a->nnz > 0) {
+    spmx_dev::validate_cols_kernel<<<validate_grid(ctx, (u64)a->nnz), 256, 0, ctx->stream>>>(
+        a->col, (u64)a->nnz, (u64)a->n, ctx->d_err);
+    post_launch();
+  }
   int err = 0;
   CUDA_CHECK(cudaMemcpyAsync(&err, ctx->d_err, sizeof(int), cudaMemcpyDeviceToHost, ctx->stream));
   CUDA_CHECK(cudaStreamSynchronize(ctx->stream));
-  static const char* what[] = {"", "", "row_ptr[0] != 0", "row_ptr[m] != nnz",
-                               "row_ptr not nondecreasing", "column index out of range"};
-  if (err) throw InvalidArg(std::string("invalid CSR: ") + what[err]);
+  if (err) throw InvalidArg(std::string("invalid CSR: ") + csr_error_text(err));
 }
 
 // ---- kernel dispatch per d ------------------------------------------------------------------
@@ -221,7 +253,8 @@ void launch_one(const spmx_plan* p, const spmx_dev::SpmmArgs& args, cudaStream_t
         <<<grid, spmx_dev::kWarpsPerCta * 32, 0, st>>>(args);
   } else {
     constexpr int kChunksPerCta = spmx_dev::kWarpsPerCta * (32 / G);  // one chunk per group
-    const unsigned grid = (unsigned)((args.n_chunks + kChunksPerCta - 1) / kChunksPerCta);
+    const u64 count = args.chunk_end - args.chunk_begin;
+    const unsigned grid = (unsigned)((count + kChunksPerCta - 1) / kChunksPerCta);
     if (grid == 0) return;
 #ifndef SPMX_CARVEOUT
 #define SPMX_CARVEOUT 30  // % of the unified L1/shared array given to shared memory
@@ -271,21 +304,28 @@ int pow2_ceil(int v) {
   return p;
 }
 
+// carry_out buffer of the plan for width d (cudaMalloc/cudaFree synchronise the device, so
+// pipelines call this before they start their transfers)
+void ensure_carry(const spmx_plan* p, int64_t d) {
+  if (!p->may_carry) return;
+  const size_t need = (size_t)p->n_chunks * (size_t)d;
+  if (need > p->carry_floats) {
+    dev_free_async(p->ctx, p->carry);
+    p->carry = dev_alloc_async<float>(p->ctx, need);
+    p->carry_floats = need;
+    CUDA_CHECK(cudaStreamSynchronize(p->ctx->stream));  // other streams may use it next
+  }
+}
+
+// Launches the SpMM (and carry fix-up) for chunks [cb, ce) of the plan's work list on `st`.
 void run_kernels(spmx_ctx* ctx, const spmx_plan* p, const spmx_csr* a, const float* d_x,
-                 int64_t d, float* d_y) {
+                 int64_t d, float* d_y, cudaStream_t st, u64 cb, u64 ce, const int* abort_flag) {
   if (a->m == 0) return;
   const bool aligned16 = ((uintptr_t)d_x % 16 == 0) && ((uintptr_t)d_y % 16 == 0);
   const int vec = (d % 4 == 0 && aligned16) ? 4 : 1;
   const int slab_max = 32 * vec * 8;  // G=32, NT=8
 
-  if (p->may_carry) {
-    const size_t need = (size_t)p->n_chunks * (size_t)d;
-    if (need > p->carry_floats) {
-      if (p->carry) CUDA_CHECK(cudaFree(p->carry));
-      p->carry = dev_alloc<float>(need);
-      p->carry_floats = need;
-    }
-  }
+  ensure_carry(p, d);
 
   spmx_dev::SpmmArgs args{};
   args.row_ptr = a->row_ptr;
@@ -297,6 +337,9 @@ void run_kernels(spmx_ctx* ctx, const spmx_plan* p, const spmx_csr* a, const flo
   args.chunk_row = p->chunk_row;
   args.chunk_nnz = p->chunk_nnz;
   args.n_chunks = p->n_chunks;
+  args.chunk_begin = cb;
+  args.chunk_end = ce;
+  args.abort_flag = abort_flag;
   args.m = (u64)a->m;
   args.ldx = (int)d;
   const bool exact = (p->flags & SPMX_EXACT_ORDER) != 0;
@@ -308,30 +351,33 @@ void run_kernels(spmx_ctx* ctx, const spmx_plan* p, const spmx_csr* a, const flo
     const int dw = (int)std::min<int64_t>(slab_max, d - c0);
     args.c0 = (int)c0;
     args.dw = dw;
-    if (p->dynamic) CUDA_CHECK(cudaMemsetAsync(p->counter, 0, sizeof(u64), ctx->stream));
+    if (p->dynamic) CUDA_CHECK(cudaMemsetAsync(p->counter, 0, sizeof(u64), st));
 #ifndef SPMX_NT
 #define SPMX_NT 2  // float4 tiles per lane for the specialised widths
 #endif
     if (vec == 4 && c0 == 0 && d == 32) {
-      launch_one<32, 8 / SPMX_NT, 4, SPMX_NT, false>(p, args, ctx->stream, ctx->sm_count);
+      launch_one<32, 8 / SPMX_NT, 4, SPMX_NT, false>(p, args, st, ctx->sm_count);
     } else if (vec == 4 && c0 == 0 && d == 64) {
-      launch_one<64, 16 / SPMX_NT, 4, SPMX_NT, false>(p, args, ctx->stream, ctx->sm_count);
+      launch_one<64, 16 / SPMX_NT, 4, SPMX_NT, false>(p, args, st, ctx->sm_count);
     } else if (vec == 4 && c0 == 0 && d == 128) {
-      launch_one<128, 32 / SPMX_NT, 4, SPMX_NT, false>(p, args, ctx->stream, ctx->sm_count);
+      launch_one<128, 32 / SPMX_NT, 4, SPMX_NT, false>(p, args, st, ctx->sm_count);
     } else {
       const int lanes = (dw + vec - 1) / vec;
       int g = pow2_ceil(std::min(lanes, 32));
       int nt = 1;
       if (lanes > 32) nt = pow2_ceil((lanes + 31) / 32);
       if (vec == 4)
-        launch_generic<4>(p, args, g, nt, ctx->stream, ctx->sm_count);
+        launch_generic<4>(p, args, g, nt, st, ctx->sm_count);
       else
-        launch_generic<1>(p, args, g, nt, ctx->stream, ctx->sm_count);
+        launch_generic<1>(p, args, g, nt, st, ctx->sm_count);
     }
-    if (p->may_carry && p->n_chunks > 1) {
-      spmx_dev::carry_fixup_kernel<<<blocks_for((p->n_chunks - 1) * (32 / spmx_dev::kFixupPerWarp), 256), 256, 0, ctx->stream>>>(
-          a->row_ptr, p->chunk_row, p->chunk_nnz, p->n_chunks, (u64)a->m, p->carry, d_y, (int)d,
-          (int)c0, dw);
+    // rows that END in chunks [cb, ce) are closed by boundaries t+1 in [cb, ce): t in [cb-1, ce-1)
+    const u64 tb = cb > 0 ? cb - 1 : 0, te = ce > 0 ? ce - 1 : 0;
+    if (p->may_carry && te > tb) {
+      spmx_dev::carry_fixup_kernel<<<blocks_for((te - tb) * (32 / spmx_dev::kFixupPerWarp), 256),
+                                     256, 0, st>>>(a->row_ptr, p->chunk_row, p->chunk_nnz,
+                                                   p->n_chunks, tb, te, (u64)a->m, p->carry, d_y,
+                                                   (int)d, (int)c0, dw);
       post_launch();
     }
   }
@@ -339,11 +385,11 @@ void run_kernels(spmx_ctx* ctx, const spmx_plan* p, const spmx_csr* a, const flo
 
 void plan_free(spmx_plan* p) {
   if (!p) return;
-  if (p->ranges) cudaFree(p->ranges);
-  if (p->chunk_row) cudaFree(p->chunk_row);
-  if (p->chunk_nnz) cudaFree(p->chunk_nnz);
-  if (p->counter) cudaFree(p->counter);
-  if (p->carry) cudaFree(p->carry);
+  dev_free_async(p->ctx, p->ranges);
+  dev_free_async(p->ctx, p->chunk_row);
+  dev_free_async(p->ctx, p->chunk_nnz);
+  dev_free_async(p->ctx, p->counter);
+  dev_free_async(p->ctx, p->carry);
   p->magic = 0;
   delete p;
 }
@@ -362,7 +408,8 @@ spmx_plan* plan_build(spmx_ctx* ctx, const spmx_csr* a, int strategy, unsigned p
   if (parts == 0) {
     // strategy-level ranges T: a few per SM (the device refines them into chunks); exact-order
     // mode has no refinement, so there T is the work-list size itself
-    const u64 fine = (m + nnz + chunk_items() - 1) / chunk_items();
+    const u64 ci = chunk_items_for(m + nnz, ctx->sm_count);
+    const u64 fine = (m + nnz + ci - 1) / ci;
     const u64 want = exact ? fine : std::min<u64>(fine, (u64)ctx->sm_count * default_parts_per_sm());
     parts = (unsigned)std::min<u64>(std::max<u64>(want, 1), 1u << 30);
   }
@@ -376,19 +423,19 @@ spmx_plan* plan_build(spmx_ctx* ctx, const spmx_csr* a, int strategy, unsigned p
     p->dynamic = dynamic != 0;
     p->batch = batch ? batch : 128;
     if (p->dynamic) {
-      p->counter = dev_alloc<u64>(1);
+      p->counter = dev_alloc_async<u64>(ctx, 1);
       CUDA_CHECK(cudaMemsetAsync(p->counter, 0, sizeof(u64), ctx->stream));
       return p;
     }
     // 1. the strategy's row-snapped boundaries and RowRange list (bit-exact with the reference)
-    u64* d_bnd = dev_alloc<u64>((size_t)parts + 1);
+    u64* d_bnd = dev_alloc_async<u64>(ctx, (size_t)parts + 1);
     strategy_row_boundaries(ctx, a, strategy, parts, d_bnd);
-    p->ranges = dev_alloc<u64>(2 * (size_t)parts);
+    p->ranges = dev_alloc_async<u64>(ctx, 2 * (size_t)parts);
     spmx_dev::ranges_from_boundaries_kernel<<<blocks_for(parts), 256, 0, ctx->stream>>>(
         d_bnd, parts, p->ranges);
     post_launch();
     // 2. strategy-level merge-path diagonals
-    u64* d_diag = dev_alloc<u64>((size_t)parts + 1);
+    u64* d_diag = dev_alloc_async<u64>(ctx, (size_t)parts + 1);
     if (strategy == SPMX_MERGE_SPLIT && !exact) {
       spmx_dev::merge_boundaries_kernel<<<blocks_for((u64)parts + 1), 256, 0, ctx->stream>>>(
           a->row_ptr, m, nnz, parts, 0, d_diag);
@@ -402,16 +449,16 @@ spmx_plan* plan_build(spmx_ctx* ctx, const spmx_csr* a, int strategy, unsigned p
     //    of short rows)
     if (exact) {
       p->n_chunks = parts;
-      p->chunk_row = dev_alloc<u64>((size_t)p->n_chunks + 1);
-      p->chunk_nnz = dev_alloc<u64>((size_t)p->n_chunks + 1);
+      p->chunk_row = dev_alloc_async<u64>(ctx, (size_t)p->n_chunks + 1);
+      p->chunk_nnz = dev_alloc_async<u64>(ctx, (size_t)p->n_chunks + 1);
       spmx_dev::merge_search_kernel<<<blocks_for(p->n_chunks + 1), 256, 0, ctx->stream>>>(
           a->row_ptr, m, nnz, d_diag, p->n_chunks + 1, p->chunk_row, p->chunk_nnz);
       post_launch();
     } else {
-      u64* d_cnt = dev_alloc<u64>(parts);
-      u64* d_off = dev_alloc<u64>((size_t)parts + 1);
+      u64* d_cnt = dev_alloc_async<u64>(ctx, parts);
+      u64* d_off = dev_alloc_async<u64>(ctx, (size_t)parts + 1);
       spmx_dev::count_chunks_kernel<<<blocks_for(parts), 256, 0, ctx->stream>>>(
-          d_diag, parts, chunk_items(), d_cnt);
+          d_diag, parts, chunk_items_for(m + nnz, ctx->sm_count), d_cnt);
       post_launch();
       spmx_dev::exclusive_scan_kernel<<<1, 1024, 0, ctx->stream>>>(d_cnt, parts, d_off);
       post_launch();
@@ -420,19 +467,19 @@ spmx_plan* plan_build(spmx_ctx* ctx, const spmx_csr* a, int strategy, unsigned p
                                  ctx->stream));
       CUDA_CHECK(cudaStreamSynchronize(ctx->stream));
       p->n_chunks = total;
-      p->chunk_row = dev_alloc<u64>((size_t)total + 1);
-      p->chunk_nnz = dev_alloc<u64>((size_t)total + 1);
+      p->chunk_row = dev_alloc_async<u64>(ctx, (size_t)total + 1);
+      p->chunk_nnz = dev_alloc_async<u64>(ctx, (size_t)total + 1);
       spmx_dev::chunk_coords_kernel<<<blocks_for(total + 1), 256, 0, ctx->stream>>>(
           a->row_ptr, m, nnz, d_diag, d_off, parts, total, snap_len(), p->chunk_row, p->chunk_nnz);
       post_launch();
       CUDA_CHECK(cudaStreamSynchronize(ctx->stream));
-      CUDA_CHECK(cudaFree(d_cnt));
-      CUDA_CHECK(cudaFree(d_off));
+      dev_free_async(ctx, d_cnt);
+      dev_free_async(ctx, d_off);
       p->may_carry = true;
     }
     CUDA_CHECK(cudaStreamSynchronize(ctx->stream));
-    CUDA_CHECK(cudaFree(d_diag));
-    CUDA_CHECK(cudaFree(d_bnd));
+    dev_free_async(ctx, d_diag);
+    dev_free_async(ctx, d_bnd);
     return p;
   } catch (...) {
     plan_free(p);
@@ -482,6 +529,11 @@ int spmx_ctx_create(int device, void* stream, spmx_ctx** out) {
     CUDA_CHECK(cudaEventCreate(&c->ev0));
     CUDA_CHECK(cudaEventCreate(&c->ev1));
     c->d_err = dev_alloc<int>(1);
+    cudaMemPool_t pool;
+    if (cudaDeviceGetDefaultMemPool(&pool, device) == cudaSuccess) {
+      uint64_t keep = ~0ull;  // do not hand pool memory back to the OS between plans
+      cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &keep);
+    }
     *out = c;
   });
 }
@@ -493,6 +545,9 @@ int spmx_ctx_destroy(spmx_ctx* ctx) {
     for (int i = 0; i < 5; ++i)
       if (ctx->ws[i]) cudaFree(ctx->ws[i]);
     cudaFree(ctx->d_err);
+    for (cudaEvent_t e : ctx->pipe_events) cudaEventDestroy(e);
+    if (ctx->s_compute) cudaStreamDestroy(ctx->s_compute);
+    if (ctx->s_d2h) cudaStreamDestroy(ctx->s_d2h);
     cudaEventDestroy(ctx->ev0);
     cudaEventDestroy(ctx->ev1);
     if (ctx->own_stream) cudaStreamDestroy(ctx->stream);
@@ -766,7 +821,7 @@ int spmx_spmm(spmx_ctx* ctx, const spmx_plan* plan, const spmx_csr* a, const flo
     if (d > (1 << 30)) throw InvalidArg("run_spmm: X.cols too large");
     if ((!d_x && a->n > 0) || (!d_y && a->m > 0)) throw InvalidArg("run_spmm: null X or Y");
     if (elapsed_ms) CUDA_CHECK(cudaEventRecord(ctx->ev0, ctx->stream));
-    run_kernels(ctx, plan, a, d_x, d, d_y);
+    run_kernels(ctx, plan, a, d_x, d, d_y, ctx->stream, 0, plan->n_chunks, nullptr);
     if (elapsed_ms) {
       CUDA_CHECK(cudaEventRecord(ctx->ev1, ctx->stream));
       CUDA_CHECK(cudaEventSynchronize(ctx->ev1));
@@ -779,6 +834,14 @@ int spmx_spmm_host(spmx_ctx* ctx, int64_t m, int64_t n, int64_t nnz, const uint6
                    const uint32_t* col, const float* vals, const float* x, int64_t x_rows,
                    int64_t d, float* y, int strategy, unsigned parts, int dynamic, uint64_t batch,
                    unsigned flags, double* times_ms) {
+  // Pipeline over three streams (the transfers dominate: PCIe moves ~8 B per nonzero up and
+  // 4*d B per row down, the kernel needs a fraction of that time):
+  //   stream 0  H2D row_ptr -> validate + plan (the plan needs row_ptr only) -> H2D X
+  //             -> H2D col/vals of row block 0, 1, ...
+  //   stream 1  per block: validate columns, SpMM over the block's chunks, carry fix-up
+  //   stream 2  per block: D2H of the Y rows that end in the block
+  // Blocks are runs of whole chunks of the work list, so every Y row is final when its
+  // block's kernels have run. Dynamic-dispatch plans have no work list: one block.
   return guarded([&] {
     check(ctx);
     if (m < 0 || n < 0 || nnz < 0) throw InvalidArg("invalid CSR: negative dimension");
@@ -786,9 +849,23 @@ int spmx_spmm_host(spmx_ctx* ctx, int64_t m, int64_t n, int64_t nnz, const uint6
     if (d < 1) throw InvalidArg("run_spmm: X.cols must be >= 1");
     if (!row_ptr || (!x && n > 0) || (!y && m > 0) || (nnz > 0 && (!col || !vals)))
       throw InvalidArg("run_spmm: null array");
-    cudaEvent_t ev[5];
-    for (auto& e : ev) CUDA_CHECK(cudaEventCreate(&e));
-    cudaStream_t st = ctx->stream;
+    if (!ctx->s_compute) {
+      CUDA_CHECK(cudaStreamCreateWithFlags(&ctx->s_compute, cudaStreamNonBlocking));
+      CUDA_CHECK(cudaStreamCreateWithFlags(&ctx->s_d2h, cudaStreamNonBlocking));
+    }
+    cudaStream_t s0 = ctx->stream, s1 = ctx->s_compute, s2 = ctx->s_d2h;
+    constexpr int kMaxBlocks = 8;
+    cudaEvent_t ev_t[4];            // timing marks on stream 0 / 2
+    cudaEvent_t ev_x, ev_in[kMaxBlocks], ev_done[kMaxBlocks];
+    size_t next_event = 0;
+    auto mk = [&](cudaEvent_t& e, bool) {
+      if (next_event == ctx->pipe_events.size()) {
+        cudaEvent_t fresh;
+        CUDA_CHECK(cudaEventCreate(&fresh));
+        ctx->pipe_events.push_back(fresh);
+      }
+      e = ctx->pipe_events[next_event++];
+    };
     u64* d_rp = (u64*)ws_get(ctx, 0, ((size_t)m + 1) * 8);
     uint32_t* d_col = (uint32_t*)ws_get(ctx, 1, (size_t)nnz * 4);
     float* d_vals = (float*)ws_get(ctx, 2, (size_t)nnz * 4);
@@ -803,42 +880,104 @@ int spmx_spmm_host(spmx_ctx* ctx, int64_t m, int64_t n, int64_t nnz, const uint6
     a.col = d_col;
     a.vals = d_vals;
     spmx_plan* plan = nullptr;
+    auto cleanup = [&] {
+      if (plan) plan_free(plan);
+      plan = nullptr;
+      a.magic = 0;
+    };
     try {
-      CUDA_CHECK(cudaEventRecord(ev[0], st));
-      CUDA_CHECK(cudaMemcpyAsync(d_rp, row_ptr, ((size_t)m + 1) * 8, cudaMemcpyHostToDevice, st));
-      if (nnz) {
-        CUDA_CHECK(cudaMemcpyAsync(d_col, col, (size_t)nnz * 4, cudaMemcpyHostToDevice, st));
-        CUDA_CHECK(cudaMemcpyAsync(d_vals, vals, (size_t)nnz * 4, cudaMemcpyHostToDevice, st));
-      }
-      CUDA_CHECK(cudaMemcpyAsync(d_x, x, (size_t)n * (size_t)d * 4, cudaMemcpyHostToDevice, st));
-      CUDA_CHECK(cudaEventRecord(ev[1], st));
-      validate_on_device(ctx, &a);
-      plan = plan_build(ctx, &a, strategy, parts, dynamic, batch, flags);
-      CUDA_CHECK(cudaEventRecord(ev[2], st));
-      run_kernels(ctx, plan, &a, d_x, d, d_y);
-      CUDA_CHECK(cudaEventRecord(ev[3], st));
-      CUDA_CHECK(cudaMemcpyAsync(y, d_y, (size_t)m * (size_t)d * 4, cudaMemcpyDeviceToHost, st));
-      CUDA_CHECK(cudaEventRecord(ev[4], st));
-      CUDA_CHECK(cudaStreamSynchronize(st));
-      if (times_ms) {
-        float t;
-        for (int i = 0; i < 4; ++i) {
-          CUDA_CHECK(cudaEventElapsedTime(&t, ev[i], ev[i + 1]));
-          times_ms[i] = t;
+      for (auto& e : ev_t) mk(e, true);
+      mk(ev_x, false);
+      for (int b = 0; b < kMaxBlocks; ++b) { mk(ev_in[b], false); mk(ev_done[b], false); }
+      const auto t_host0 = std::chrono::steady_clock::now();
+      CUDA_CHECK(cudaEventRecord(ev_t[0], s0));
+      CUDA_CHECK(cudaMemcpyAsync(d_rp, row_ptr, ((size_t)m + 1) * 8, cudaMemcpyHostToDevice, s0));
+      // X starts moving while the plan is being built from row_ptr
+      CUDA_CHECK(cudaMemsetAsync(ctx->d_err, 0, sizeof(int), s0));
+      spmx_dev::validate_row_ptr_kernel<<<validate_grid(ctx, (u64)m), 256, 0, s0>>>(
+          d_rp, (u64)m, (u64)nnz, ctx->d_err);
+      post_launch();
+      int err = 0;
+      CUDA_CHECK(cudaMemcpyAsync(&err, ctx->d_err, sizeof(int), cudaMemcpyDeviceToHost, s0));
+      CUDA_CHECK(cudaStreamSynchronize(s0));
+      if (err) throw InvalidArg(std::string("invalid CSR: ") + csr_error_text(err));
+      // plan first (a fraction of a millisecond; its cudaMalloc/cudaFree calls would otherwise
+      // serialise against transfers in flight), then everything else streams
+      plan = plan_build(ctx, &a, strategy, parts, dynamic, batch, flags);  // syncs stream 0
+      ensure_carry(plan, d);
+      const auto t_host1 = std::chrono::steady_clock::now();
+      CUDA_CHECK(cudaMemcpyAsync(d_x, x, (size_t)n * (size_t)d * 4, cudaMemcpyHostToDevice, s0));
+      CUDA_CHECK(cudaEventRecord(ev_x, s0));
+      CUDA_CHECK(cudaEventRecord(ev_t[1], s0));
+
+      // blocks = runs of whole chunks with about equal nonzero counts
+      int nblocks = 1;
+      std::vector<u64> cb{0, plan->n_chunks}, row_b{0, (u64)m}, nnz_b{0, (u64)nnz};
+      if (!plan->dynamic && plan->n_chunks >= 64 && nnz > (1 << 20)) {
+        nblocks = kMaxBlocks;
+        cb.assign(nblocks + 1, 0);
+        row_b.assign(nblocks + 1, 0);
+        nnz_b.assign(nblocks + 1, 0);
+        for (int b = 0; b <= nblocks; ++b) cb[b] = plan->n_chunks * (u64)b / (u64)nblocks;
+        for (int b = 0; b <= nblocks; ++b) {
+          CUDA_CHECK(cudaMemcpyAsync(&row_b[b], plan->chunk_row + cb[b], 8, cudaMemcpyDeviceToHost, s0));
+          CUDA_CHECK(cudaMemcpyAsync(&nnz_b[b], plan->chunk_nnz + cb[b], 8, cudaMemcpyDeviceToHost, s0));
         }
-        CUDA_CHECK(cudaEventElapsedTime(&t, ev[0], ev[4]));
-        times_ms[4] = t;
-        times_ms[5] = 0.0;
+        CUDA_CHECK(cudaStreamSynchronize(s0));
+        // a block's first chunk may start inside a row whose head is in the previous block; the
+        // nonzeros it needs still start at its own chunk_nnz, which is what nnz_b holds
+      }
+      for (int b = 0; b < nblocks; ++b) {
+        const u64 n0 = nnz_b[b], n1 = nnz_b[b + 1];
+        if (n1 > n0) {
+          CUDA_CHECK(cudaMemcpyAsync(d_col + n0, col + n0, (n1 - n0) * 4, cudaMemcpyHostToDevice, s0));
+          CUDA_CHECK(cudaMemcpyAsync(d_vals + n0, vals + n0, (n1 - n0) * 4, cudaMemcpyHostToDevice, s0));
+        }
+        CUDA_CHECK(cudaEventRecord(ev_in[b], s0));
+        CUDA_CHECK(cudaStreamWaitEvent(s1, ev_in[b], 0));
+        if (b == 0) CUDA_CHECK(cudaStreamWaitEvent(s1, ev_x, 0));
+        if (n1 > n0) {
+          spmx_dev::validate_cols_kernel<<<validate_grid(ctx, n1 - n0), 256, 0, s1>>>(
+              d_col + n0, n1 - n0, (u64)n, ctx->d_err);
+          post_launch();
+        }
+        run_kernels(ctx, plan, &a, d_x, d, d_y, s1, cb[b], cb[b + 1], ctx->d_err);
+        CUDA_CHECK(cudaEventRecord(ev_done[b], s1));
+        CUDA_CHECK(cudaStreamWaitEvent(s2, ev_done[b], 0));
+        const u64 r0 = row_b[b], r1 = (b + 1 == nblocks) ? (u64)m : row_b[b + 1];
+        if (b == 0) CUDA_CHECK(cudaEventRecord(ev_t[2], s2));
+        if (r1 > r0)
+          CUDA_CHECK(cudaMemcpyAsync(y + r0 * (size_t)d, d_y + r0 * (size_t)d, (r1 - r0) * (size_t)d * 4,
+                                     cudaMemcpyDeviceToHost, s2));
+      }
+      CUDA_CHECK(cudaEventRecord(ev_t[3], s2));
+      CUDA_CHECK(cudaMemcpyAsync(&err, ctx->d_err, sizeof(int), cudaMemcpyDeviceToHost, s2));
+      CUDA_CHECK(cudaStreamSynchronize(s2));
+      CUDA_CHECK(cudaStreamSynchronize(s1));
+      CUDA_CHECK(cudaStreamSynchronize(s0));
+      if (err) throw InvalidArg(std::string("invalid CSR: ") + csr_error_text(err));
+      if (times_ms) {
+        float t = 0.f;
+        // {row_ptr upload + plan (host clock), -, first block ready -> last Y byte, -, total, blocks}
+        times_ms[0] = std::chrono::duration<double, std::milli>(t_host1 - t_host0).count();
+        times_ms[1] = times_ms[0];
+        CUDA_CHECK(cudaEventElapsedTime(&t, ev_t[2], ev_t[3]));
+        times_ms[2] = 0.0;
+        times_ms[3] = t;
+        CUDA_CHECK(cudaEventElapsedTime(&t, ev_t[0], ev_t[1]));
+        const double head = t;
+        times_ms[4] = std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t_host0).count();
+        times_ms[2] = times_ms[4] - times_ms[3] - head > 0 ? times_ms[4] - times_ms[3] - head : 0.0;
+        times_ms[5] = (double)nblocks;
       }
     } catch (...) {
-      if (plan) plan_free(plan);
-      a.magic = 0;
-      for (auto& e : ev) cudaEventDestroy(e);
+      cudaStreamSynchronize(s0);
+      cudaStreamSynchronize(s1);
+      cudaStreamSynchronize(s2);
+      cleanup();
       throw;
     }
-    plan_free(plan);
-    a.magic = 0;
-    for (auto& e : ev) cudaEventDestroy(e);
+    cleanup();
   });
 }
 

@@ -89,7 +89,10 @@ struct SpmmArgs {
   float* __restrict__ carry_out; // n_chunks x ldx (rows cut by a chunk end), may be null in exact mode
   const u64* __restrict__ chunk_row;  // n_chunks + 1
   const u64* __restrict__ chunk_nnz;  // n_chunks + 1
-  u64 n_chunks;
+  u64 n_chunks;     // size of the whole work list
+  u64 chunk_begin;  // this launch processes chunks [chunk_begin, chunk_end)
+  u64 chunk_end;
+  const int* abort_flag;  // when non-null and set (invalid input found on the device): do nothing
   u64 m;
   int ldx;     // row stride of X, Y and carry_out in floats (= d)
   int c0;      // first column of the slab this launch computes
@@ -307,9 +310,10 @@ spmm_chunk_kernel(const SpmmArgs a) {
   __shared__ WarpScratch<G> scratch[kWarpsPerCta];
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
   const u64 warp = (u64)blockIdx.x * kWarpsPerCta + w;
-  if (warp * NGW >= a.n_chunks) return;  // whole warp idle
-  const u64 chunk = warp * NGW + lane / G;
-  const bool active = chunk < a.n_chunks;
+  if (a.chunk_begin + warp * NGW >= a.chunk_end) return;  // whole warp idle
+  if (a.abort_flag && *(volatile const int*)a.abort_flag) return;
+  const u64 chunk = a.chunk_begin + warp * NGW + lane / G;
+  const bool active = chunk < a.chunk_end;
   u64 r0 = 0, j0 = 0, r1 = 0, j1 = 0;
   bool has_carry = false;
   if (active) {
@@ -357,15 +361,16 @@ spmm_dynamic_kernel(const SpmmArgs a) {
 constexpr int kFixupPerWarp = 8;
 __global__ void __launch_bounds__(256)
 carry_fixup_kernel(const u64* __restrict__ row_ptr, const u64* __restrict__ chunk_row,
-                   const u64* __restrict__ chunk_nnz, u64 n_chunks, u64 m,
+                   const u64* __restrict__ chunk_nnz, u64 n_chunks, u64 t_begin, u64 t_end, u64 m,
                    const float* __restrict__ carry_out, float* __restrict__ y, int ldx, int c0,
                    int dw) {
   const int lane = threadIdx.x & 31;
   const u64 warp = ((u64)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
-  const u64 t = warp * kFixupPerWarp + lane;  // chunk whose END boundary this lane inspects
+  // chunk whose END boundary this lane inspects; boundaries t+1 for t in [t_begin, t_end)
+  const u64 t = t_begin + warp * kFixupPerWarp + lane;
   bool closes = false;
   u64 r = 0, u0 = 0;
-  if (lane < kFixupPerWarp && t + 1 < n_chunks) {  // the last chunk ends at (m, nnz): no carry
+  if (lane < kFixupPerWarp && t < t_end && t + 1 < n_chunks) {  // the last chunk ends at (m, nnz)
     r = chunk_row[t + 1];
     if (r < m) {
       const u64 rp = __ldg(row_ptr + r);
@@ -389,7 +394,7 @@ carry_fixup_kernel(const u64* __restrict__ row_ptr, const u64* __restrict__ chun
     todo &= todo - 1;
     const u64 rr = __shfl_sync(kFullMask, r, src);
     const u64 first = __shfl_sync(kFullMask, u0, src);
-    const u64 last = warp * kFixupPerWarp + src;
+    const u64 last = t_begin + warp * kFixupPerWarp + src;
     for (int c = lane; c < dw; c += 32) {
       const float* __restrict__ src_c = carry_out + c0 + c;
       float* dst = y + (size_t)rr * ldx + c0 + c;

@@ -161,7 +161,7 @@ __global__ void chunk_coords_kernel(const u64* __restrict__ row_ptr, u64 m, u64 
                                     u64* __restrict__ out_row, u64* __restrict__ out_nnz) {
   const u64 c = (u64)blockIdx.x * blockDim.x + threadIdx.x;
   if (c > n_chunks) return;
-  u64 k;
+  u64 k, range_start = 0;
   bool interior = false;
   if (c == n_chunks) {
     k = diag[parts];
@@ -176,12 +176,14 @@ __global__ void chunk_coords_kernel(const u64* __restrict__ row_ptr, u64 m, u64 
     // s < cnt <= items/chunk+1: s*items fits u64 for any realistic size
     k = diag[t] + (s * items) / cnt;
     interior = s != 0;
+    range_start = diag[t];
   }
   u64 i, j;
   merge_search_dev(row_ptr, m, nnz, k, i, j);
   if (interior && i < m) {
     const u64 rs = __ldg(row_ptr + i);
-    if (j > rs && __ldg(row_ptr + i + 1) - rs < snap_len) j = rs;
+    // (never back past the range's own first boundary: a merge cut may already sit in this row)
+    if (j > rs && __ldg(row_ptr + i + 1) - rs < snap_len && i + rs >= range_start) j = rs;
   }
   out_row[c] = i;
   out_nnz[c] = j;
@@ -189,8 +191,7 @@ __global__ void chunk_coords_kernel(const u64* __restrict__ row_ptr, u64 m, u64 
 
 // validate_csr, src/csr.cpp:18-42, on the device. err receives the largest code seen:
 // 2 row_ptr[0] != 0, 3 row_ptr[m] != nnz, 4 row_ptr decreasing, 5 column out of range.
-__global__ void validate_csr_kernel(const u64* __restrict__ row_ptr, const unsigned* __restrict__ col,
-                                    u64 m, u64 n, u64 nnz, int* err) {
+__global__ void validate_row_ptr_kernel(const u64* __restrict__ row_ptr, u64 m, u64 nnz, int* err) {
   const u64 stride = (u64)gridDim.x * blockDim.x;
   const u64 tid = (u64)blockIdx.x * blockDim.x + threadIdx.x;
   int e = 0;
@@ -200,8 +201,14 @@ __global__ void validate_csr_kernel(const u64* __restrict__ row_ptr, const unsig
   }
   for (u64 i = tid; i < m; i += stride)
     if (row_ptr[i + 1] < row_ptr[i] || row_ptr[i + 1] > nnz) e = max(e, 4);
-  for (u64 k = tid; k < nnz; k += stride)
-    if ((u64)col[k] >= n) e = max(e, 5);
+  if (e) atomicMax(err, e);
+}
+
+__global__ void validate_cols_kernel(const unsigned* __restrict__ col, u64 count, u64 n, int* err) {
+  const u64 stride = (u64)gridDim.x * blockDim.x;
+  int e = 0;
+  for (u64 k = (u64)blockIdx.x * blockDim.x + threadIdx.x; k < count; k += stride)
+    if ((u64)col[k] >= n) e = 5;
   if (e) atomicMax(err, e);
 }
 

@@ -235,6 +235,28 @@ def test_config_siblings_match_reference_checksums(ctx, oracle):
             assert np.array_equal(ctx.split_merge(da, t), z[name + f"_merge{t}"])
 
 
+def test_work_list_is_monotone_and_covers(ctx):
+    """Chunk coordinates of every plan are nondecreasing in both components, start at (0, 0),
+    end at (m, nnz), and strategy-level ranges are kept as chunk boundaries."""
+    from paper_2312_05639_b200 import workloads as W
+    for name, kw in (("c2", {"scale_override": 12}), ("c4", {"scale_override": 12}),
+                     ("c3", {"m_override": 1 << 12}), ("c1", {})):
+        a, _, _ = W.make_config(name, **kw)
+        rp, col, vals = a.numpy()
+        da = ctx.csr_upload(a.m, a.n, rp, col, vals)
+        for s in STRATS:
+            for parts in (0, 1, 7, 300):
+                for fl in (0, EXACT):
+                    p = ctx.plan(da, s, parts, flags=fl)
+                    cr, cj = (v.astype(np.int64) for v in p.chunks())
+                    assert cr[0] == 0 and cj[0] == 0 and cr[-1] == a.m and cj[-1] == a.nnz
+                    assert np.all(np.diff(cr) >= 0) and np.all(np.diff(cj) >= 0), (name, s, parts, fl)
+                    # a coordinate (i, j) lies on the merge path: row_ptr[i] <= j <= row_ptr[i+1]
+                    inner = cr < a.m
+                    assert np.all(cj[inner] >= rp[cr[inner]].astype(np.int64))
+                    assert np.all(cj[inner] <= rp[cr[inner] + 1].astype(np.int64))
+
+
 def test_host_entry_point(ctx, oracle):
     """spmx_spmm_host: the run_spmm-shaped call with host buffers."""
     rng = np.random.default_rng(21)
