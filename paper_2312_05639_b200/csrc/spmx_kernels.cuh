@@ -50,9 +50,45 @@ struct VecT<4> {
   float v[4];
 };
 
+// Optional L2 eviction policies (createpolicy): evict_last for X rows, evict_first for the
+// col/val stream and Y. Measured on c2/c3: no effect (X's L2 misses are not caused by the
+// streams), so they are compiled out by default; -DSPMX_POL_X=1 etc. re-enable them.
+#ifndef SPMX_POL_X
+#define SPMX_POL_X 0
+#endif
+#ifndef SPMX_POL_STREAM
+#define SPMX_POL_STREAM 0
+#endif
+#ifndef SPMX_POL_Y
+#define SPMX_POL_Y 0
+#endif
+__device__ __forceinline__ u64 policy_evict_first() {
+  u64 p;
+  asm("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(p));
+  return p;
+}
+__device__ __forceinline__ u64 policy_evict_last() {
+  u64 p;
+  asm("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(p));
+  return p;
+}
+
 template <int VEC>
-__device__ __forceinline__ VecT<VEC> ld_x(const float* p) {
+__device__ __forceinline__ VecT<VEC> ld_x(const float* p, u64 pol) {
   VecT<VEC> r;
+#if SPMX_POL_X
+  if constexpr (VEC == 4) {
+    asm volatile("ld.global.nc.L2::cache_hint.v4.f32 {%0,%1,%2,%3}, [%4], %5;"
+                 : "=f"(r.v[0]), "=f"(r.v[1]), "=f"(r.v[2]), "=f"(r.v[3])
+                 : "l"(p), "l"(pol));
+  } else if constexpr (VEC == 2) {
+    asm volatile("ld.global.nc.L2::cache_hint.v2.f32 {%0,%1}, [%2], %3;"
+                 : "=f"(r.v[0]), "=f"(r.v[1])
+                 : "l"(p), "l"(pol));
+  } else {
+    asm volatile("ld.global.nc.L2::cache_hint.f32 %0, [%1], %2;" : "=f"(r.v[0]) : "l"(p), "l"(pol));
+  }
+#else
   if constexpr (VEC == 4) {
     float4 t = __ldg(reinterpret_cast<const float4*>(p));
     r.v[0] = t.x; r.v[1] = t.y; r.v[2] = t.z; r.v[3] = t.w;
@@ -62,7 +98,28 @@ __device__ __forceinline__ VecT<VEC> ld_x(const float* p) {
   } else {
     r.v[0] = __ldg(p);
   }
+#endif
   return r;
+}
+
+// streaming loads of the CSR arrays
+__device__ __forceinline__ u32 ld_stream(const u32* p, u64 pol) {
+#if SPMX_POL_STREAM
+  u32 v;
+  asm volatile("ld.global.nc.L1::no_allocate.L2::cache_hint.b32 %0, [%1], %2;" : "=r"(v) : "l"(p), "l"(pol));
+  return v;
+#else
+  return __ldcs(p);
+#endif
+}
+__device__ __forceinline__ float ld_stream(const float* p, u64 pol) {
+#if SPMX_POL_STREAM
+  float v;
+  asm volatile("ld.global.nc.L1::no_allocate.L2::cache_hint.f32 %0, [%1], %2;" : "=f"(v) : "l"(p), "l"(pol));
+  return v;
+#else
+  return __ldcs(p);
+#endif
 }
 
 __device__ __forceinline__ void prefetch_l2(const void* p) {
@@ -70,7 +127,19 @@ __device__ __forceinline__ void prefetch_l2(const void* p) {
 }
 
 template <int VEC>
-__device__ __forceinline__ void st_y(float* p, const float* a) {
+__device__ __forceinline__ void st_y(float* p, const float* a, u64 pol) {
+#if SPMX_POL_Y
+  if constexpr (VEC == 4) {
+    asm volatile("st.global.L2::cache_hint.v4.f32 [%0], {%1,%2,%3,%4}, %5;" ::"l"(p), "f"(a[0]), "f"(a[1]),
+                 "f"(a[2]), "f"(a[3]), "l"(pol)
+                 : "memory");
+  } else if constexpr (VEC == 2) {
+    asm volatile("st.global.L2::cache_hint.v2.f32 [%0], {%1,%2}, %3;" ::"l"(p), "f"(a[0]), "f"(a[1]), "l"(pol)
+                 : "memory");
+  } else {
+    asm volatile("st.global.L2::cache_hint.f32 [%0], %1, %2;" ::"l"(p), "f"(a[0]), "l"(pol) : "memory");
+  }
+#else
   if constexpr (VEC == 4) {
     __stcs(reinterpret_cast<float4*>(p), make_float4(a[0], a[1], a[2], a[3]));
   } else if constexpr (VEC == 2) {
@@ -78,6 +147,7 @@ __device__ __forceinline__ void st_y(float* p, const float* a) {
   } else {
     __stcs(p, a[0]);
   }
+#endif
 }
 
 struct SpmmArgs {
@@ -105,11 +175,11 @@ struct SpmmArgs {
 
 template <int G, int VEC, int NT, bool RAGGED>
 __device__ __forceinline__ void store_row(const SpmmArgs& a, float* dst_row, int lg,
-                                          const float (&acc)[NT][VEC]) {
+                                          const float (&acc)[NT][VEC], u64 pol) {
 #pragma unroll
   for (int t = 0; t < NT; ++t) {
     const int c = (t * G + lg) * VEC;
-    if (!RAGGED || c < a.dw) st_y<VEC>(dst_row + a.c0 + c, acc[t]);
+    if (!RAGGED || c < a.dw) st_y<VEC>(dst_row + a.c0 + c, acc[t], pol);
   }
 }
 
@@ -182,6 +252,7 @@ __device__ __forceinline__ void process_piece(const SpmmArgs& a, bool active, u6
   u32* __restrict__ s_end = sm.row_end[g];
   unsigned short* __restrict__ s_idx = sm.row_idx[g];
   float acc[NT][VEC];
+  const u64 pol_first = policy_evict_first(), pol_last = policy_evict_last();
 
   u32 ws = 0;  // nonzero offset where the current window starts
   for (u64 wbase = r0; __any_sync(kFullMask, wbase < row_lim); wbase += W) {
@@ -216,7 +287,7 @@ __device__ __forceinline__ void process_piece(const SpmmArgs& a, bool active, u6
           em &= em - 1;
           const u64 rr = wbase + q0 + src;
           float* dst = (rr < r1) ? a.y + (size_t)rr * (size_t)ldx : carry_row;
-          store_row<G, VEC, NT, RAGGED>(a, dst, lg, acc);
+          store_row<G, VEC, NT, RAGGED>(a, dst, lg, acc, pol_first);
         }
       }
     }
@@ -232,8 +303,8 @@ __device__ __forceinline__ void process_piece(const SpmmArgs& a, bool active, u6
     // ---- walk the window's nonzeros ---------------------------------------------------------
     u32 c0 = 0, c1 = 0;
     float v0 = 0.0f, v1 = 0.0f;
-    if ((u32)lg < L) { c0 = __ldcs(colp + p0 + lg); v0 = __ldcs(valp + p0 + lg); }
-    if ((u32)(G + lg) < L) { c1 = __ldcs(colp + p0 + G + lg); v1 = __ldcs(valp + p0 + G + lg); }
+    if ((u32)lg < L) { c0 = ld_stream(colp + p0 + lg, pol_first); v0 = ld_stream(valp + p0 + lg, pol_first); }
+    if ((u32)(G + lg) < L) { c1 = ld_stream(colp + p0 + G + lg, pol_first); v1 = ld_stream(valp + p0 + G + lg, pol_first); }
     VecT<VEC> xv[U][NT];
 #pragma unroll
     for (int u = 0; u < U; ++u) {
@@ -242,7 +313,7 @@ __device__ __forceinline__ void process_piece(const SpmmArgs& a, bool active, u6
         const float* xr = xbase + (size_t)kq * (size_t)ldx;
 #pragma unroll
         for (int t = 0; t < NT; ++t)
-          if (!RAGGED || (t * G + lg) * VEC < a.dw) xv[u][t] = ld_x<VEC>(xr + t * G * VEC);
+          if (!RAGGED || (t * G + lg) * VEC < a.dw) xv[u][t] = ld_x<VEC>(xr + t * G * VEC, pol_last);
       }
     }
 #ifndef SPMX_PF
@@ -258,8 +329,8 @@ __device__ __forceinline__ void process_piece(const SpmmArgs& a, bool active, u6
       u32 c2 = 0;
       float v2 = 0.0f;
       if (nb + 2 * G + lg < L) {
-        c2 = __ldcs(colp + p0 + nb + 2 * G + lg);
-        v2 = __ldcs(valp + p0 + nb + 2 * G + lg);
+        c2 = ld_stream(colp + p0 + nb + 2 * G + lg, pol_first);
+        v2 = ld_stream(valp + p0 + nb + 2 * G + lg, pol_first);
       }
       if (SPMX_PF > 0 && nb + SPMX_PF + lg < L) {  // DRAM latency is paid here, off the critical path
         prefetch_l2(colp + p0 + nb + SPMX_PF + lg);
@@ -283,16 +354,20 @@ __device__ __forceinline__ void process_piece(const SpmmArgs& a, bool active, u6
         if (--left == 0) {  // row k ends here: store it, start the next one
           const u64 rr = wbase + s_idx[k];
           float* dst = (rr < r1) ? a.y + (size_t)rr * (size_t)ldx : carry_row;
-          store_row<G, VEC, NT, RAGGED>(a, dst, lg, acc);
+          store_row<G, VEC, NT, RAGGED>(a, dst, lg, acc, pol_first);
           zero_acc(acc);
           ++k;
           left = (k < count) ? s_end[k] - s_end[k - 1] : 0x7fffffffu;
         }
         if (nb + t + U < L) {
+#ifdef SPMX_EXP_HOTX
+          const float* xr = xbase + (size_t)(kq & (SPMX_EXP_HOTX - 1)) * (size_t)ldx;
+#else
           const float* xr = xbase + (size_t)kq * (size_t)ldx;
+#endif
 #pragma unroll
           for (int tt = 0; tt < NT; ++tt)
-            if (!RAGGED || (tt * G + lg) * VEC < a.dw) xv[u][tt] = ld_x<VEC>(xr + tt * G * VEC);
+            if (!RAGGED || (tt * G + lg) * VEC < a.dw) xv[u][tt] = ld_x<VEC>(xr + tt * G * VEC, pol_last);
         }
       }
       c0 = c1; v0 = v1;
