@@ -356,7 +356,7 @@ void run_kernels(spmx_ctx* ctx, const spmx_plan* p, const spmx_csr* a, const flo
 #define SPMX_NT 2  // float4 tiles per lane for the specialised widths
 #endif
     if (vec == 4 && c0 == 0 && d == 32) {
-      launch_one<32, 8 / SPMX_NT, 4, SPMX_NT, false>(p, args, st, ctx->sm_count);
+      launch_one<32, 8, 4, 1, false>(p, args, st, ctx->sm_count);  // see Tune<32, 1>
     } else if (vec == 4 && c0 == 0 && d == 64) {
       launch_one<64, 16 / SPMX_NT, 4, SPMX_NT, false>(p, args, st, ctx->sm_count);
     } else if (vec == 4 && c0 == 0 && d == 128) {

@@ -198,6 +198,20 @@ __device__ __forceinline__ void zero_acc(float (&acc)[NT][VEC]) {
 #define SPMX_MIN_CTAS 2
 #endif
 
+// Per-width tuning (measured on B200, tools/dev_bench.py): CTAs per SM the register budget is
+// set for, and LDG.128 gathers in flight per lane. Narrow rows (d = 32: one 128-byte line per
+// row) do better with more resident warps and a shallower pipeline.
+template <int D_CT, int NT>
+struct Tune {
+  static constexpr int kMinCtas = (NT <= 2) ? SPMX_MIN_CTAS : 1;
+  static constexpr int kInFlight = SPMX_U;
+};
+template <>
+struct Tune<32, 1> {
+  static constexpr int kMinCtas = 3;
+  static constexpr int kInFlight = 8;
+};
+
 // Rows whose bounds one group stages at a time (shared memory: 6 bytes per row and group).
 template <int G>
 struct Window {
@@ -238,7 +252,7 @@ __device__ __forceinline__ void process_piece(const SpmmArgs& a, bool active, u6
                                               int lane, WarpScratch<G>& sm) {
   constexpr int NGW = 32 / G;
   constexpr int W = Window<G>::kRows;
-  constexpr int UMAX = (SPMX_U / NT) > 0 ? (SPMX_U / NT) : 1;
+  constexpr int UMAX = (Tune<D_CT, NT>::kInFlight / NT) > 0 ? (Tune<D_CT, NT>::kInFlight / NT) : 1;
   constexpr int U = UMAX < G ? UMAX : G;  // gathers in flight per lane; divides G
   const int g = lane / G, lg = lane % G;
   const int ldx = D_CT ? D_CT : a.ldx;
@@ -379,7 +393,7 @@ __device__ __forceinline__ void process_piece(const SpmmArgs& a, bool active, u6
 
 // Static work list: group s of the grid (G lanes) owns chunk s.
 template <int D_CT, int G, int VEC, int NT, bool RAGGED>
-__global__ void __launch_bounds__(kWarpsPerCta * 32, (NT <= 2 ? SPMX_MIN_CTAS : 1))
+__global__ void __launch_bounds__(kWarpsPerCta * 32, Tune<D_CT, NT>::kMinCtas)
 spmm_chunk_kernel(const SpmmArgs a) {
   constexpr int NGW = 32 / G;
   __shared__ WarpScratch<G> scratch[kWarpsPerCta];
@@ -408,7 +422,7 @@ spmm_chunk_kernel(const SpmmArgs a) {
 // covering [0, m) exactly as the reference's dispatcher does; the claimed rows are dealt
 // to the warp's groups in equal contiguous shares (rows are never split).
 template <int D_CT, int G, int VEC, int NT, bool RAGGED>
-__global__ void __launch_bounds__(kWarpsPerCta * 32, (NT <= 2 ? SPMX_MIN_CTAS : 1))
+__global__ void __launch_bounds__(kWarpsPerCta * 32, Tune<D_CT, NT>::kMinCtas)
 spmm_dynamic_kernel(const SpmmArgs a) {
   constexpr int NGW = 32 / G;
   __shared__ WarpScratch<G> scratch[kWarpsPerCta];
