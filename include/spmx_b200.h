@@ -50,7 +50,11 @@ extern "C" {
                                granularity; split rows are summed from per-chunk partials in CSR
                                order (deterministic, within the north_star tolerance), all other
                                rows stay bitwise equal. */
-#define SPMX_NO_COOP 2u     /* disable the intra-warp cooperative path for long row segments */
+#define SPMX_NO_COOP 2u     /* reserved (no effect) */
+#define SPMX_JIT_WIDTH 4u   /* instantiate the kernel for exactly this d at run time (NVRTC, cached
+                               per d and device) instead of using the runtime-d kernels: the GPU
+                               counterpart of the reference's per-d code generation
+                               (plan.cpp:80-93, jit.cpp:136-154). d = 32/64/128 are precompiled. */
 
 typedef struct spmx_ctx spmx_ctx;   /* one per (device, stream) */
 typedef struct spmx_csr spmx_csr;   /* A resident on the device */
@@ -147,6 +151,10 @@ int spmx_spmm_reference(spmx_ctx* ctx, const spmx_csr* a, const float* d_x, int6
 /* max_relative_error (executor.cpp:27-34): max_i |y_i - ref_i| / max(|ref_i|, 1e-6) */
 int spmx_max_relative_error(spmx_ctx* ctx, const float* d_y, const float* d_ref, size_t count,
                             double* out);
+
+/* run-time code generation counters (RunReport.codegen_s of the reference, executor.cpp:54-60):
+ * kernels compiled so far in this process and the seconds spent compiling them */
+int spmx_jit_stats(uint64_t* kernels_compiled, double* seconds);
 
 /* ---- helpers for the reference's report fields ---------------------------------------------- */
 /* checksum(Y), dense.cpp:17-28, of a device buffer (FNV-1a is sequential: the buffer is copied

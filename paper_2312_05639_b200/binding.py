@@ -25,6 +25,7 @@ ROW, NNZ, MERGE = 0, 1, 2
 STRATEGY = {"row": ROW, "nnz": NNZ, "merge": MERGE}
 EXACT_ORDER = 1
 NO_COOP = 2
+JIT_WIDTH = 4
 
 NVCC_FLAGS = ["-gencode", "arch=compute_100a,code=sm_100a", "-lineinfo", "-O3", "-std=c++17",
               "-Xcompiler", "-fPIC", "-shared"]
@@ -42,14 +43,30 @@ class SpmxLogicError(RuntimeError):
     """SPMX_ELOGIC — where the reference throws std::logic_error."""
 
 
+KERNEL_SRC_INC = os.path.join(CSRC, "spmx_kernels_src.inc")
+
+
+def generate_kernel_source_include() -> None:
+    """The kernel header as a C++ raw string literal, compiled into the library so that
+    spmx_spmm can instantiate the kernel for any d at run time with NVRTC (the GPU role of the
+    reference's emit(), src/jit.cpp:136-154)."""
+    src = open(os.path.join(CSRC, "spmx_kernels.cuh")).read()
+    assert ')SPMXSRC"' not in src
+    text = 'R"SPMXSRC(' + src + ')SPMXSRC"\n'
+    if not os.path.exists(KERNEL_SRC_INC) or open(KERNEL_SRC_INC).read() != text:
+        with open(KERNEL_SRC_INC, "w") as f:
+            f.write(text)
+
+
 def build_library(force: bool = False, verbose: bool = False) -> str:
     """Compile csrc/*.cu into libspmx_b200.so for sm_100a (nvcc cross-compiles without a GPU)."""
     srcs = [os.path.join(CSRC, f) for f in sorted(os.listdir(CSRC)) if f.endswith(".cu")]
-    deps = [os.path.join(CSRC, f) for f in os.listdir(CSRC)] + [HEADER]
+    deps = [os.path.join(CSRC, f) for f in os.listdir(CSRC) if not f.endswith(".inc")] + [HEADER]
     if not force and os.path.exists(LIB_PATH):
         if os.path.getmtime(LIB_PATH) >= max(os.path.getmtime(d) for d in deps):
             return LIB_PATH
-    cmd = ["nvcc", *NVCC_FLAGS, "-o", LIB_PATH, *srcs]
+    generate_kernel_source_include()
+    cmd = ["nvcc", *NVCC_FLAGS, "-o", LIB_PATH, *srcs, "-ldl"]
     if verbose:
         print(" ".join(cmd), file=sys.stderr)
     subprocess.check_call(cmd)
@@ -115,6 +132,7 @@ class Lib:
         L.spmx_checksum_device.argtypes = [vp, vp, sz, P(u64)]
         L.spmx_spmm_reference.argtypes = [vp, vp, vp, i64, i64, vp]
         L.spmx_max_relative_error.argtypes = [vp, vp, vp, sz, P(C.c_double)]
+        L.spmx_jit_stats.argtypes = [P(u64), P(C.c_double)]
 
     def check(self, rc: int):
         if rc == 0:
@@ -122,6 +140,12 @@ class Lib:
         msg = self.lib.spmx_last_error().decode(errors="replace")
         raise {1: SpmxInvalidArgument, 2: SpmxRuntimeError, 3: SpmxLogicError}.get(
             rc, SpmxRuntimeError)(msg)
+
+    def jit_stats(self):
+        """(number of per-d kernels compiled at run time, total seconds spent compiling)."""
+        n, t = C.c_uint64(), C.c_double()
+        self.lib.spmx_jit_stats(C.byref(n), C.byref(t))
+        return n.value, t.value
 
     def launch_count(self) -> int:
         return int(self.lib.spmx_kernel_launch_count())

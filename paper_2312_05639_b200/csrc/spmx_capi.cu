@@ -19,6 +19,7 @@
 #include <string>
 #include <vector>
 
+#include "spmx_jit.cuh"
 #include "spmx_kernels.cuh"
 #include "spmx_partition.cuh"
 
@@ -346,6 +347,35 @@ void run_kernels(spmx_ctx* ctx, const spmx_plan* p, const spmx_csr* a, const flo
   args.long_seg = (exact || (p->flags & SPMX_NO_COOP)) ? 0u : long_seg();
   args.counter = p->counter;
   args.batch = p->batch;
+
+  // run-time instantiation for exactly this d (SPMX_JIT_WIDTH): one launch covers the whole
+  // width when it fits 32 lanes x 8 tiles; the precompiled widths and dynamic plans keep
+  // their own kernels
+  const bool precompiled = vec == 4 && (d == 32 || d == 64 || d == 128);
+  if ((p->flags & SPMX_JIT_WIDTH) && !p->dynamic && !precompiled && d <= spmx_jit::max_width(vec)) {
+    int dev = 0;
+    CUDA_CHECK(cudaGetDevice(&dev));
+    const spmx_jit::Kernel& k = spmx_jit::get(dev, (int)d, vec);
+    args.c0 = 0;
+    args.dw = (int)d;
+    const int chunks_per_cta = spmx_dev::kWarpsPerCta * (32 / k.shape.g);
+    const unsigned grid = (unsigned)((ce - cb + chunks_per_cta - 1) / chunks_per_cta);
+    if (grid) {
+      void* kargs[] = {(void*)&args};
+      CUDA_CHECK(cudaLaunchKernel((const void*)k.chunk, dim3(grid), dim3(spmx_dev::kWarpsPerCta * 32),
+                                  kargs, 0, st));
+      post_launch();
+    }
+    const u64 tb = cb > 0 ? cb - 1 : 0, te = ce > 0 ? ce - 1 : 0;
+    if (p->may_carry && te > tb) {
+      spmx_dev::carry_fixup_kernel<<<blocks_for((te - tb) * (32 / spmx_dev::kFixupPerWarp), 256),
+                                     256, 0, st>>>(a->row_ptr, p->chunk_row, p->chunk_nnz,
+                                                   p->n_chunks, tb, te, (u64)a->m, p->carry, d_y,
+                                                   (int)d, 0, (int)d);
+      post_launch();
+    }
+    return;
+  }
 
   for (int64_t c0 = 0; c0 < d; c0 += slab_max) {
     const int dw = (int)std::min<int64_t>(slab_max, d - c0);
@@ -1012,6 +1042,14 @@ int spmx_max_relative_error(spmx_ctx* ctx, const float* d_y, const float* d_ref,
     CUDA_CHECK(cudaStreamSynchronize(ctx->stream));
     CUDA_CHECK(cudaFree(d_bits));
     std::memcpy(out, &bits, 8);
+  });
+}
+
+int spmx_jit_stats(uint64_t* kernels_compiled, double* seconds) {
+  return guarded([&] {
+    std::lock_guard<std::mutex> lock(spmx_jit::mu());
+    if (kernels_compiled) *kernels_compiled = spmx_jit::stats().compiled;
+    if (seconds) *seconds = spmx_jit::stats().seconds;
   });
 }
 

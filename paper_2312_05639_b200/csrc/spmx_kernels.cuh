@@ -19,10 +19,10 @@
 // gathered), bounded by L2->SM / L1 gather bandwidth, not by math.
 #pragma once
 
+#ifndef __CUDACC_RTC__  // NVRTC (runtime per-d instantiation) has the CUDA builtins predeclared
 #include <cuda_runtime.h>
 #include <stdint.h>
-
-#include <type_traits>
+#endif
 
 namespace spmx_dev {
 
@@ -212,6 +212,12 @@ struct Tune<32, 1> {
   static constexpr int kInFlight = 8;
 };
 
+__host__ __device__ constexpr int pipeline_depth(int want, int g) {
+  int u = 1;
+  while (u * 2 <= want && u * 2 <= g) u *= 2;
+  return u;
+}
+
 // Rows whose bounds one group stages at a time (shared memory: 6 bytes per row and group).
 template <int G>
 struct Window {
@@ -250,10 +256,10 @@ template <int D_CT, int G, int VEC, int NT, bool RAGGED>
 __device__ __forceinline__ void process_piece(const SpmmArgs& a, bool active, u64 r0, u64 j0,
                                               u64 r1, u64 j1, bool has_carry, float* carry_row,
                                               int lane, WarpScratch<G>& sm) {
-  constexpr int NGW = 32 / G;
   constexpr int W = Window<G>::kRows;
-  constexpr int UMAX = (Tune<D_CT, NT>::kInFlight / NT) > 0 ? (Tune<D_CT, NT>::kInFlight / NT) : 1;
-  constexpr int U = UMAX < G ? UMAX : G;  // gathers in flight per lane; divides G
+  // positions in flight per lane: the largest power of two with U * NT <= kInFlight, at most G
+  // (so that U divides G and a position keeps its pipeline slot from batch to batch)
+  constexpr int U = pipeline_depth(Tune<D_CT, NT>::kInFlight / NT, G);
   const int g = lane / G, lg = lane % G;
   const int ldx = D_CT ? D_CT : a.ldx;
   const u64 row_lim = active ? r1 + (has_carry ? 1 : 0) : r0;

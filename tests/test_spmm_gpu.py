@@ -295,3 +295,26 @@ def test_device_reference_and_error_metric(ctx, oracle):
     ctx.synchronize()
     got = ctx.max_relative_error(y, yr)
     assert got == oracle.max_relative_error(y.cpu().numpy(), want)
+
+
+@pytest.mark.parametrize("d", [1, 20, 45, 48, 96, 100, 256, 1000])
+def test_runtime_instantiation_per_width(ctx, oracle, d):
+    """SPMX_JIT_WIDTH: the kernel is compiled for exactly this d at run time (NVRTC) — the GPU
+    counterpart of the reference's emit(). Same bits as the precompiled path."""
+    from paper_2312_05639_b200.binding import JIT_WIDTH, Lib
+    rng = np.random.default_rng(500 + d)
+    m, n = 211, 137
+    rp, col, vals = rand_csr(rng, m, n, 0.12)
+    x = (rng.random((n, d), np.float32) * 2 - 1).astype(np.float32)
+    want = oracle.spmm_fused(m, n, rp, col, vals, x)
+    unf = oracle.spmm_unfused(m, n, rp, col, vals, x)
+    bound = oracle.abs_bound(m, rp, col, vals, x)
+    before = Lib.get().jit_stats()
+    for s in STRATS:
+        y, _ = run(ctx, m, n, rp, col, vals, x, s, 5, EXACT | JIT_WIDTH)
+        assert np.array_equal(y.view(np.uint32), want.view(np.uint32)), (d, s)
+        y, _ = run(ctx, m, n, rp, col, vals, x, s, 0, JIT_WIDTH)
+        assert north_star_ok(y, unf, bound), (d, s)
+    after = Lib.get().jit_stats()
+    assert after[0] >= before[0] and after[0] >= 1   # compiled once per (device, d), then cached
+    assert after[0] - before[0] <= 1

@@ -13,7 +13,7 @@ import torch
 
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 from paper_2312_05639_b200 import workloads as W  # noqa: E402
-from paper_2312_05639_b200.binding import Context, EXACT_ORDER, NO_COOP  # noqa: E402
+from paper_2312_05639_b200.binding import Context, EXACT_ORDER, NO_COOP, JIT_WIDTH  # noqa: E402
 
 
 def main():
@@ -24,6 +24,7 @@ def main():
     ap.add_argument("--iters", type=int, default=20)
     ap.add_argument("--check", action="store_true")
     ap.add_argument("--parts", type=int, default=0)
+    ap.add_argument("--d", type=int, default=None, help="override the dense width")
     ap.add_argument("--modes", default="fast,exact")
     args = ap.parse_args()
     peak = 6551.0
@@ -36,6 +37,10 @@ def main():
         t0 = time.time()
         a, x, spec = W.make_config(name, device="cuda", scale_override=args.scale, m_override=args.m)
         torch.cuda.synchronize()
+        if args.d:
+            spec["d"] = args.d
+            x = W.dense(a.n, args.d, spec["seed"], spec["x_dist"], "cuda")
+            torch.cuda.synchronize()
         d = spec["d"]
         byts = W.algorithmic_bytes(a.m, a.n, a.nnz, d)
         print(f"== {name}: m={a.m} nnz={a.nnz} d={d} bytes={byts/1e6:.1f}MB gen={time.time()-t0:.1f}s "
@@ -45,7 +50,7 @@ def main():
         ref = None
         for strat in ("row", "nnz", "merge", "row-dyn"):
             for mode in args.modes.split(","):
-                flags = {"fast": 0, "exact": EXACT_ORDER, "nocoop": NO_COOP}[mode]
+                flags = {"fast": 0, "exact": EXACT_ORDER, "nocoop": NO_COOP, "jit": JIT_WIDTH}[mode]
                 dyn = strat == "row-dyn"
                 tp = time.time()
                 p = ctx.plan(da, strat.split("-")[0], args.parts, dynamic=dyn, flags=flags)
