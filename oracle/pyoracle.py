@@ -250,6 +250,12 @@ class RefLib:
         L.ref_csr_copy.argtypes = [vp, _u64p, _u32p, _f32p]
         L.ref_csr_copy.restype = None
         L.ref_random_dense.argtypes = [i64, i64, u64, _f32p]
+        L.ref_save_csr_cache.argtypes = [vp, C.c_char_p]
+        L.ref_load_csr_cache.argtypes = [C.c_char_p]
+        L.ref_load_csr_cache.restype = vp
+        L.ref_load_matrix_market.argtypes = [C.c_char_p]
+        L.ref_load_matrix_market.restype = vp
+        L.ref_write_matrix_market.argtypes = [vp, C.c_char_p]
 
     def _chk(self, rc):
         if rc != 0:
@@ -330,6 +336,24 @@ class RefLib:
 
     def random_csr(self, rows, avg, skew, seed) -> RefCsr:
         return RefCsr(self, self.lib.ref_random_csr(rows, avg, skew, seed))
+
+    def save_csr_cache(self, a: RefCsr, path):
+        self._chk(self.lib.ref_save_csr_cache(a.h, path.encode()))
+
+    def load_csr_cache(self, path) -> RefCsr:
+        h = self.lib.ref_load_csr_cache(path.encode())
+        if not h:
+            raise RefError(2, self.lib.ref_last_error().decode())
+        return RefCsr(self, h)
+
+    def load_matrix_market(self, path) -> RefCsr:
+        h = self.lib.ref_load_matrix_market(path.encode())
+        if not h:
+            raise RefError(2, self.lib.ref_last_error().decode())
+        return RefCsr(self, h)
+
+    def write_matrix_market(self, a: RefCsr, path):
+        self._chk(self.lib.ref_write_matrix_market(a.h, path.encode()))
 
     def random_dense(self, rows, cols, seed):
         out = np.zeros((rows, cols), np.float32)

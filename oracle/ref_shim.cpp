@@ -23,6 +23,7 @@
 #include "spmx/csr.hpp"
 #include "spmx/dense.hpp"
 #include "spmx/executor.hpp"
+#include "spmx/mmio.hpp"
 #include "spmx/partition.hpp"
 #include "spmx/reference.hpp"
 
@@ -229,6 +230,24 @@ void ref_csr_copy(void* h, uint64_t* row_ptr, uint32_t* col, float* vals) {
     std::memcpy(col, a.col_indices.data(), a.col_indices.size() * sizeof(uint32_t));
   if (!a.vals.empty()) std::memcpy(vals, a.vals.data(), a.vals.size() * sizeof(float));
 }
+// ---- file formats (csr.cpp:65-104, mmio.cpp:20-110) ----------------------------------
+int ref_save_csr_cache(void* h, const char* path) {
+  return guarded([&] { spmx::save_csr_cache(static_cast<Holder*>(h)->a, path); });
+}
+void* ref_load_csr_cache(const char* path) {
+  Holder* h = nullptr;
+  if (guarded([&] { h = new Holder; h->a = spmx::load_csr_cache(path); }) != 0) { delete h; return nullptr; }
+  return h;
+}
+void* ref_load_matrix_market(const char* path) {
+  Holder* h = nullptr;
+  if (guarded([&] { h = new Holder; h->a = spmx::load_matrix_market(path); }) != 0) { delete h; return nullptr; }
+  return h;
+}
+int ref_write_matrix_market(void* h, const char* path) {
+  return guarded([&] { spmx::write_matrix_market(static_cast<Holder*>(h)->a, path); });
+}
+
 int ref_random_dense(int64_t rows, int64_t cols, uint64_t seed, float* out) {
   return guarded([&] {
     spmx::DenseMatrix x = spmx::random_dense(rows, cols, seed);

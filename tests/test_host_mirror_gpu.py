@@ -9,7 +9,7 @@ pytestmark = pytest.mark.gpu
 
 
 def test_cpp_host_mirror_cases():
-    from paper_2312_05639_b200 import hostbuild
+    from tools import hostbuild
     exe = hostbuild.BIN
     if not os.path.exists(exe):
         exe = hostbuild.build_host_tests()
