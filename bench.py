@@ -117,18 +117,21 @@ def cpu_reference_run(rp, col, vals, xn, m, n, strategy, trials, warm=1):
     Returns (gflops_from_mean_time, times_s, kind, cores)."""
     from oracle.pyoracle import Oracle, RefLib
     nnz, d = int(rp[m]), xn.shape[1]
+    # all host threads, stated explicitly: torchrun exports OMP_NUM_THREADS=1, which would
+    # otherwise make the reference's "threads = 0 -> omp_get_max_threads()" single-threaded
+    host_threads = len(os.sched_getaffinity(0)) if hasattr(os, "sched_getaffinity") else (os.cpu_count() or 1)
     if RefLib.available():
         ref = RefLib()
         a = ref.csr(m, n, rp, col, vals)
         dyn = strategy == "row"  # the reference's default and fastest row-split mode
-        _, rep = ref.run_spmm(a, xn, strategy, dyn, 0, "native", 128, warm + trials)
+        _, rep = ref.run_spmm(a, xn, strategy, dyn, host_threads, "native", 128, warm + trials)
         times = rep["times_s"][warm:]
         return 2.0 * nnz * d / (sum(times) / len(times)) / 1e9, times, "reference", rep["threads"]
     orc = Oracle()
     times = []
     for i in range(warm + trials):
         t0 = time.perf_counter()
-        orc.spmm_fused(m, n, rp, col, vals, xn, threads=0)
+        orc.spmm_fused(m, n, rp, col, vals, xn, threads=host_threads)
         if i >= warm:
             times.append(time.perf_counter() - t0)
     return 2.0 * nnz * d / (sum(times) / len(times)) / 1e9, times, "port", orc.last_threads
@@ -193,11 +196,20 @@ def main():
     from paper_2312_05639_b200.binding import Context, EXACT_ORDER, Lib
 
     assert torch.cuda.is_available(), "bench.py needs a CUDA device: there is no CPU fallback"
+    # SPMX_BENCH_SHARE_GPU=1 (debug): all ranks use cuda:0 and rendezvous over gloo, to exercise
+    # the N>1 code path on a one-GPU box. The ranks' kernels are independent (row shards), none
+    # waits on another. Numbers from such a run are not multi-GPU numbers.
+    share_gpu = os.environ.get("SPMX_BENCH_SHARE_GPU") == "1"
+    if share_gpu:
+        local_rank = 0
     torch.cuda.set_device(local_rank)
     dev = torch.device("cuda", local_rank)
     if world > 1:
         os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
-        dist.init_process_group("nccl", device_id=dev)
+        if share_gpu:
+            dist.init_process_group("gloo")
+        else:
+            dist.init_process_group("nccl", device_id=dev)
     name = args.workload or ("c2" if world == 1 else "c5")
     flags = EXACT_ORDER if args.exact else 0
     lib = Lib.get()
@@ -226,6 +238,8 @@ def main():
         e0.record(); sharding.broadcast_x(x, 0); e1.record(); torch.cuda.synchronize()
         bcast_ms = sharding.max_over_ranks(e0.elapsed_time(e1), dev)
         extra.update({"parallelism": f"row-shard{world}", "shard_rows": [rb, re], "x_broadcast_ms": bcast_ms})
+        if share_gpu:
+            extra["debug"] = "SPMX_BENCH_SHARE_GPU: all ranks on one GPU over gloo (code-path check only)"
         nnz_total = int(sharding.sum_over_ranks(a.nnz, dev))
         m_total = int(sharding.sum_over_ranks(a.m, dev))
     else:
