@@ -63,10 +63,6 @@ int guarded(F&& f) {
 
 constexpr uint32_t kMagicCtx = 0x58435443, kMagicCsr = 0x58435352, kMagicPlan = 0x58504c4e;
 constexpr u64 kDefaultChunkItems = 256;  // merge items (rows + nonzeros) per warp-level chunk
-#ifndef SPMX_LONG_SEG
-#define SPMX_LONG_SEG 256
-#endif
-constexpr unsigned kDefaultLongSeg = SPMX_LONG_SEG;  // row segments >= this are shared by the warp's groups
 
 // tuning knobs, overridable from the environment for experiments (tools/dev_bench.py)
 inline u64 env_u64(const char* name, u64 dflt) {
@@ -79,7 +75,6 @@ inline u64 chunk_items_for(u64 items, int sm_count) {
   const u64 want_chunks = (u64)sm_count * 64;
   return std::min<u64>(chunk_items(), std::max<u64>(32, items / want_chunks));
 }
-inline unsigned long_seg() { return (unsigned)env_u64("SPMX_LONG_SEG", kDefaultLongSeg); }
 // interior chunk boundaries never cut a row shorter than this
 inline u64 snap_len() { return env_u64("SPMX_SNAP_LEN", 128); }
 inline u64 default_parts_per_sm() { return env_u64("SPMX_PARTS_PER_SM", 8); }
@@ -343,8 +338,6 @@ void run_kernels(spmx_ctx* ctx, const spmx_plan* p, const spmx_csr* a, const flo
   args.abort_flag = abort_flag;
   args.m = (u64)a->m;
   args.ldx = (int)d;
-  const bool exact = (p->flags & SPMX_EXACT_ORDER) != 0;
-  args.long_seg = (exact || (p->flags & SPMX_NO_COOP)) ? 0u : long_seg();
   args.counter = p->counter;
   args.batch = p->batch;
 

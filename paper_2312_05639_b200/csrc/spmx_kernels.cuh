@@ -122,10 +122,6 @@ __device__ __forceinline__ float ld_stream(const float* p, u64 pol) {
 #endif
 }
 
-__device__ __forceinline__ void prefetch_l2(const void* p) {
-  asm volatile("prefetch.global.L2 [%0];" ::"l"(p));
-}
-
 template <int VEC>
 __device__ __forceinline__ void st_y(float* p, const float* a, u64 pol) {
 #if SPMX_POL_Y
@@ -167,7 +163,6 @@ struct SpmmArgs {
   int ldx;     // row stride of X, Y and carry_out in floats (= d)
   int c0;      // first column of the slab this launch computes
   int dw;      // slab width in columns (<= G*VEC*NT)
-  u32 long_seg;  // row segments at least this long take the cooperative path (0 = never)
   // dynamic row dispatch (persistent CTAs claim `batch` rows at a time)
   u64* counter;
   u64 batch;
@@ -336,14 +331,6 @@ __device__ __forceinline__ void process_piece(const SpmmArgs& a, bool active, u6
           if (!RAGGED || (t * G + lg) * VEC < a.dw) xv[u][t] = ld_x<VEC>(xr + t * G * VEC, pol_last);
       }
     }
-#ifndef SPMX_PF
-#define SPMX_PF 96  // positions ahead at which the col/val stream is pulled into L2
-#endif
-    if (SPMX_PF > 0) {  // the first lines of the stream
-#pragma unroll
-      for (int q = 2 * G; q < SPMX_PF; q += G)
-        if ((u32)(q + lg) < L) { prefetch_l2(colp + p0 + q + lg); prefetch_l2(valp + p0 + q + lg); }
-    }
 #pragma unroll 1
     for (u32 nb = 0; nb < Lmax; nb += G) {
       u32 c2 = 0;
@@ -352,10 +339,7 @@ __device__ __forceinline__ void process_piece(const SpmmArgs& a, bool active, u6
         c2 = ld_stream(colp + p0 + nb + 2 * G + lg, pol_first);
         v2 = ld_stream(valp + p0 + nb + 2 * G + lg, pol_first);
       }
-      if (SPMX_PF > 0 && nb + SPMX_PF + lg < L) {  // DRAM latency is paid here, off the critical path
-        prefetch_l2(colp + p0 + nb + SPMX_PF + lg);
-        prefetch_l2(valp + p0 + nb + SPMX_PF + lg);
-      }
+
 #pragma unroll
       for (int t = 0; t < G; ++t) {
         const int u = t % U;
@@ -380,11 +364,7 @@ __device__ __forceinline__ void process_piece(const SpmmArgs& a, bool active, u6
           left = (k < count) ? s_end[k] - s_end[k - 1] : 0x7fffffffu;
         }
         if (nb + t + U < L) {
-#ifdef SPMX_EXP_HOTX
-          const float* xr = xbase + (size_t)(kq & (SPMX_EXP_HOTX - 1)) * (size_t)ldx;
-#else
           const float* xr = xbase + (size_t)kq * (size_t)ldx;
-#endif
 #pragma unroll
           for (int tt = 0; tt < NT; ++tt)
             if (!RAGGED || (tt * G + lg) * VEC < a.dw) xv[u][tt] = ld_x<VEC>(xr + tt * G * VEC, pol_last);
