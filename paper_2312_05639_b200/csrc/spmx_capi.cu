@@ -233,10 +233,6 @@ void validate_on_device(spmx_ctx* ctx, const spmx_csr* a) {
 }
 
 // ---- kernel dispatch per d ------------------------------------------------------------------
-struct Shape {
-  int d_ct, g, vec, nt;
-};
-
 template <int D_CT, int G, int VEC, int NT, bool RAGGED>
 void launch_one(const spmx_plan* p, const spmx_dev::SpmmArgs& args, cudaStream_t st, int sm_count) {
   if (p->dynamic) {

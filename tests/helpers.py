@@ -25,7 +25,6 @@ def exact_cover(ranges, m):
 def rand_csr(rng, m, n, density, dup=False):
     """Random rectangular CSR, sorted duplicate-free columns per row (like
     tests/oracles.hpp:53-72 but numpy-seeded)."""
-    rows = []
     rp = [0]
     cols, vals = [], []
     for _ in range(m):
