@@ -123,6 +123,10 @@ struct spmx_plan {
   u64* ranges = nullptr;     // 2*parts, device (absent under dynamic dispatch)
   u64* chunk_row = nullptr;  // n_chunks+1
   u64* chunk_nnz = nullptr;  // n_chunks+1
+  uint32_t* chain_first = nullptr;  // n_chunks: start of the carry chain closed by boundary t+1
+  uint32_t* long_buf = nullptr;     // [count | boundaries closing chains longer than kLongChain]
+  uint32_t* long_list = nullptr;    // = long_buf + 1
+  uint32_t n_long = 0;
   u64* counter = nullptr;    // dynamic dispatch
   bool may_carry = false;
   mutable float* carry = nullptr;  // n_chunks x ld floats, grown on demand
@@ -309,6 +313,32 @@ void ensure_carry(const spmx_plan* p, int64_t d) {
   }
 }
 
+// carry_fixup_kernel over boundaries t+1, t in [tb, te), with the widest column vector the
+// slab's alignment allows.
+void launch_fixup(const spmx_plan* p, u64 tb, u64 te, float* d_y, int ldx, int c0, int dw,
+                  cudaStream_t st) {
+  const bool a16 = ((uintptr_t)d_y % 16 == 0) && ldx % 4 == 0 && c0 % 4 == 0 && dw % 4 == 0;
+  const bool a8 = ((uintptr_t)d_y % 8 == 0) && ldx % 2 == 0 && c0 % 2 == 0 && dw % 2 == 0;
+  const int vec = a16 ? 4 : a8 ? 2 : 1;
+  int lpc = 1;  // lanes per chain: enough to cover the slab once, at most a warp
+  while (lpc < 32 && lpc * vec < dw) lpc *= 2;
+  constexpr int kT = spmx_dev::kFixupThreads;
+  const unsigned grid = p->n_long + blocks_for((te - tb) * (u64)lpc, kT);
+  if (vec == 4)
+    spmx_dev::carry_fixup_kernel<4><<<grid, kT, 0, st>>>(p->chain_first, p->chunk_row, p->long_list,
+                                                          p->n_long, tb, te, p->carry, d_y, ldx,
+                                                          c0, dw, lpc);
+  else if (vec == 2)
+    spmx_dev::carry_fixup_kernel<2><<<grid, kT, 0, st>>>(p->chain_first, p->chunk_row, p->long_list,
+                                                          p->n_long, tb, te, p->carry, d_y, ldx,
+                                                          c0, dw, lpc);
+  else
+    spmx_dev::carry_fixup_kernel<1><<<grid, kT, 0, st>>>(p->chain_first, p->chunk_row, p->long_list,
+                                                          p->n_long, tb, te, p->carry, d_y, ldx,
+                                                          c0, dw, lpc);
+  post_launch();
+}
+
 // Launches the SpMM (and carry fix-up) for chunks [cb, ce) of the plan's work list on `st`.
 void run_kernels(spmx_ctx* ctx, const spmx_plan* p, const spmx_csr* a, const float* d_x,
                  int64_t d, float* d_y, cudaStream_t st, u64 cb, u64 ce, const int* abort_flag) {
@@ -357,11 +387,7 @@ void run_kernels(spmx_ctx* ctx, const spmx_plan* p, const spmx_csr* a, const flo
     }
     const u64 tb = cb > 0 ? cb - 1 : 0, te = ce > 0 ? ce - 1 : 0;
     if (p->may_carry && te > tb) {
-      spmx_dev::carry_fixup_kernel<<<blocks_for((te - tb) * (32 / spmx_dev::kFixupPerWarp), 256),
-                                     256, 0, st>>>(a->row_ptr, p->chunk_row, p->chunk_nnz,
-                                                   p->n_chunks, tb, te, (u64)a->m, p->carry, d_y,
-                                                   (int)d, 0, (int)d);
-      post_launch();
+      launch_fixup(p, tb, te, d_y, (int)d, 0, (int)d, st);
     }
     return;
   }
@@ -393,11 +419,7 @@ void run_kernels(spmx_ctx* ctx, const spmx_plan* p, const spmx_csr* a, const flo
     // rows that END in chunks [cb, ce) are closed by boundaries t+1 in [cb, ce): t in [cb-1, ce-1)
     const u64 tb = cb > 0 ? cb - 1 : 0, te = ce > 0 ? ce - 1 : 0;
     if (p->may_carry && te > tb) {
-      spmx_dev::carry_fixup_kernel<<<blocks_for((te - tb) * (32 / spmx_dev::kFixupPerWarp), 256),
-                                     256, 0, st>>>(a->row_ptr, p->chunk_row, p->chunk_nnz,
-                                                   p->n_chunks, tb, te, (u64)a->m, p->carry, d_y,
-                                                   (int)d, (int)c0, dw);
-      post_launch();
+      launch_fixup(p, tb, te, d_y, (int)d, (int)c0, dw, st);
     }
   }
 }
@@ -406,6 +428,8 @@ void plan_free(spmx_plan* p) {
   if (!p) return;
   dev_free_async(p->ctx, p->ranges);
   dev_free_async(p->ctx, p->chunk_row);
+  dev_free_async(p->ctx, p->chain_first);
+  dev_free_async(p->ctx, p->long_buf);
   dev_free_async(p->ctx, p->chunk_nnz);
   dev_free_async(p->ctx, p->counter);
   dev_free_async(p->ctx, p->carry);
@@ -491,6 +515,19 @@ spmx_plan* plan_build(spmx_ctx* ctx, const spmx_csr* a, int strategy, unsigned p
       spmx_dev::chunk_coords_kernel<<<blocks_for(total + 1), 256, 0, ctx->stream>>>(
           a->row_ptr, m, nnz, d_diag, d_off, parts, total, snap_len(), p->chunk_row, p->chunk_nnz);
       post_launch();
+      if (total >= 0xffffffffull) throw InvalidArg("plan: work list too long");
+      p->chain_first = dev_alloc_async<uint32_t>(ctx, (size_t)total);
+      // long_list[0] doubles as the counter while the list is built: [count | entries...]
+      const size_t long_cap = (size_t)(total / spmx_dev::kLongChain) + 1;
+      p->long_buf = dev_alloc_async<uint32_t>(ctx, long_cap + 1);
+      p->long_list = p->long_buf + 1;
+      CUDA_CHECK(cudaMemsetAsync(p->long_buf, 0, sizeof(uint32_t), ctx->stream));
+      spmx_dev::chain_first_kernel<<<blocks_for(total), 256, 0, ctx->stream>>>(
+          a->row_ptr, p->chunk_row, p->chunk_nnz, total, m, p->chain_first, p->long_list,
+          p->long_buf);
+      post_launch();
+      CUDA_CHECK(cudaMemcpyAsync(&p->n_long, p->long_buf, sizeof(uint32_t), cudaMemcpyDeviceToHost,
+                                 ctx->stream));
       CUDA_CHECK(cudaStreamSynchronize(ctx->stream));
       dev_free_async(ctx, d_cnt);
       dev_free_async(ctx, d_off);

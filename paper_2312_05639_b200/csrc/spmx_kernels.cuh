@@ -30,7 +30,10 @@ typedef unsigned long long u64;
 typedef unsigned int u32;
 
 constexpr unsigned kFullMask = 0xffffffffu;
-constexpr int kWarpsPerCta = 8;
+#ifndef SPMX_WARPS_PER_CTA
+#define SPMX_WARPS_PER_CTA 2  // small CTAs: a finished warp frees its slot at once (measured best)
+#endif
+constexpr int kWarpsPerCta = SPMX_WARPS_PER_CTA;
 
 // ---- cache-policy-aware loads/stores ---------------------------------------------------
 // X rows are the only data with reuse: read-only path, default (allocating) L1 policy.
@@ -42,11 +45,11 @@ struct VecT<1> {
   float v[1];
 };
 template <>
-struct VecT<2> {
+struct alignas(8) VecT<2> {
   float v[2];
 };
 template <>
-struct VecT<4> {
+struct alignas(16) VecT<4> {
   float v[4];
 };
 
@@ -192,18 +195,22 @@ __device__ __forceinline__ void zero_acc(float (&acc)[NT][VEC]) {
 #ifndef SPMX_MIN_CTAS
 #define SPMX_MIN_CTAS 2
 #endif
+#ifndef SPMX_STAGE_BATCH
+#define SPMX_STAGE_BATCH 4  // row_ptr loads in flight per lane while staging row bounds
+#endif
+constexpr int kStageBatch = SPMX_STAGE_BATCH;
 
 // Per-width tuning (measured on B200, tools/dev_bench.py): CTAs per SM the register budget is
 // set for, and LDG.128 gathers in flight per lane. Narrow rows (d = 32: one 128-byte line per
 // row) do better with more resident warps and a shallower pipeline.
 template <int D_CT, int NT>
 struct Tune {
-  static constexpr int kMinCtas = (NT <= 2) ? SPMX_MIN_CTAS : 1;
+  static constexpr int kMinCtas = ((NT <= 2) ? SPMX_MIN_CTAS : 1) * (8 / kWarpsPerCta);
   static constexpr int kInFlight = SPMX_U;
 };
 template <>
 struct Tune<32, 1> {
-  static constexpr int kMinCtas = 3;
+  static constexpr int kMinCtas = 3 * (8 / kWarpsPerCta);
   static constexpr int kInFlight = 8;
 };
 
@@ -230,7 +237,7 @@ struct WarpScratch {
 
 // One piece of the merge path per GROUP of G lanes: the nonzeros and row ends between the
 // coordinates (r0, j0) and (r1, j1). Rows [r0, r1) end inside the piece and are stored to Y;
-// when the piece ends in the middle of row r1 (has_carry) the partial sum of that row's
+// when the piece ends in the middle of row r1 (r1 < m) the partial sum of that row's
 // nonzeros [.., j1) goes to carry_row. A row whose head lies in an earlier piece is stored
 // like any other row; carry_fixup_kernel adds the earlier partials afterwards, in CSR order.
 // The 32/G groups of a warp run the same instruction stream on different pieces (all loop
@@ -249,7 +256,7 @@ struct WarpScratch {
 // A piece must span fewer than 2^32 nonzeros (the plan guarantees it).
 template <int D_CT, int G, int VEC, int NT, bool RAGGED>
 __device__ __forceinline__ void process_piece(const SpmmArgs& a, bool active, u64 r0, u64 j0,
-                                              u64 r1, u64 j1, bool has_carry, float* carry_row,
+                                              u64 r1, u64 j1, float* carry_row,
                                               int lane, WarpScratch<G>& sm) {
   constexpr int W = Window<G>::kRows;
   // positions in flight per lane: the largest power of two with U * NT <= kInFlight, at most G
@@ -257,7 +264,8 @@ __device__ __forceinline__ void process_piece(const SpmmArgs& a, bool active, u6
   constexpr int U = pipeline_depth(Tune<D_CT, NT>::kInFlight / NT, G);
   const int g = lane / G, lg = lane % G;
   const int ldx = D_CT ? D_CT : a.ldx;
-  const u64 row_lim = active ? r1 + (has_carry ? 1 : 0) : r0;
+  // row r1 is staged too: clipped to the piece it is empty unless the piece ends inside it
+  const u64 row_lim = active ? r1 + (r1 < a.m ? 1 : 0) : r0;
   const u32* __restrict__ colp = a.col + j0;
   const float* __restrict__ valp = a.vals + j0;
   const float* __restrict__ xbase = a.x + a.c0 + lg * VEC;
@@ -272,37 +280,56 @@ __device__ __forceinline__ void process_piece(const SpmmArgs& a, bool active, u6
   u32 ws = 0;  // nonzero offset where the current window starts
   for (u64 wbase = r0; __any_sync(kFullMask, wbase < row_lim); wbase += W) {
     const int nw = wbase < row_lim ? (int)min((u64)W, row_lim - wbase) : 0;
+    // The window's first two column/value batches do not depend on the row bounds: fetch them
+    // now so that their latency overlaps the row_ptr loads below.
+    const u32 p0 = ws;
+    u32 c0 = 0, c1 = 0;
+    float v0 = 0.0f, v1 = 0.0f;
+    if (p0 + lg < span) { c0 = ld_stream(colp + p0 + lg, pol_first); v0 = ld_stream(valp + p0 + lg, pol_first); }
+    if (p0 + G + lg < span) { c1 = ld_stream(colp + p0 + G + lg, pol_first); v1 = ld_stream(valp + p0 + G + lg, pol_first); }
     // ---- stage the window: clipped row ends, compacted over non-empty rows ----------------
+    // Row ends are loaded kStageBatch * G rows at a time (all loads of a batch in flight
+    // together); a row starts where the previous one ends.
     int count = 0;
+    u32 prev_e = ws;
     __syncwarp();
     zero_acc(acc);
     const int nw_max = __reduce_max_sync(kFullMask, nw);
 #pragma unroll 1
-    for (int q0 = 0; q0 < nw_max; q0 += G) {
-      const int li = q0 + lg;
-      u32 s = 0, e = 0;
-      const bool valid = li < nw;
-      if (valid) {
-        const u64 lo = __ldg(a.row_ptr + wbase + li), hi = __ldg(a.row_ptr + wbase + li + 1);
-        s = lo > j0 ? (u32)min(lo - j0, (u64)span) : 0u;
-        e = hi > j0 ? (u32)min(hi - j0, (u64)span) : 0u;
+    for (int qb = 0; qb < nw_max; qb += kStageBatch * G) {
+      u32 eb[kStageBatch];
+#pragma unroll
+      for (int i = 0; i < kStageBatch; ++i) {
+        const int li = qb + i * G + lg;
+        eb[i] = 0;
+        if (li < nw) {
+          const u64 hi = __ldg(a.row_ptr + wbase + li + 1);
+          eb[i] = hi > j0 ? (u32)min(hi - j0, (u64)span) : 0u;
+        }
       }
-      const unsigned ne = __ballot_sync(kFullMask, valid && e != s) & grp_mask;
-      if (valid && e != s) {
-        const int pos = count + __popc(ne & lt_mask);
-        s_idx[pos] = (unsigned short)li;
-        s_end[pos] = e;
-      }
-      count += __popc(ne);
-      // empty rows: the whole group writes one row of zeros at a time
-      unsigned em = __ballot_sync(kFullMask, valid && e == s) & grp_mask;
-      while (__any_sync(kFullMask, em != 0)) {
-        if (em) {
+#pragma unroll
+      for (int i = 0; i < kStageBatch; ++i) {
+        const int q0 = qb + i * G;
+        if (q0 >= nw_max) break;  // warp-uniform
+        const int li = q0 + lg;
+        const bool valid = li < nw;
+        const u32 e = eb[i];
+        const u32 up = __shfl_up_sync(kFullMask, e, 1, G);
+        const u32 s = lg == 0 ? prev_e : up;
+        prev_e = __shfl_sync(kFullMask, e, G - 1, G);
+        const unsigned ne = __ballot_sync(kFullMask, valid && e != s) & grp_mask;
+        if (valid && e != s) {
+          const int pos = count + __popc(ne & lt_mask);
+          s_idx[pos] = (unsigned short)li;
+          s_end[pos] = e;
+        }
+        count += __popc(ne);
+        // empty rows that end inside the piece: the whole group writes one row of zeros at a time
+        unsigned em = __ballot_sync(kFullMask, valid && e == s && wbase + li < r1) & grp_mask;
+        while (em) {
           const int src = (__ffs(em) - 1) - g * G;
           em &= em - 1;
-          const u64 rr = wbase + q0 + src;
-          float* dst = (rr < r1) ? a.y + (size_t)rr * (size_t)ldx : carry_row;
-          store_row<G, VEC, NT, RAGGED>(a, dst, lg, acc, pol_first);
+          store_row<G, VEC, NT, RAGGED>(a, a.y + (size_t)(wbase + q0 + src) * (size_t)ldx, lg, acc, pol_first);
         }
       }
     }
@@ -311,15 +338,10 @@ __device__ __forceinline__ void process_piece(const SpmmArgs& a, bool active, u6
     const u32 L = we - ws;  // nonzeros of this window in this group's piece
     const u32 Lmax = __reduce_max_sync(kFullMask, L);
     if (Lmax == 0) continue;  // warp-uniform
-    const u32 p0 = ws;
     int k = 0;  // current row = k-th non-empty row of the window
     u32 left = (L > 0) ? s_end[0] - p0 : 0x7fffffffu;  // nonzeros left in the current row
 
     // ---- walk the window's nonzeros ---------------------------------------------------------
-    u32 c0 = 0, c1 = 0;
-    float v0 = 0.0f, v1 = 0.0f;
-    if ((u32)lg < L) { c0 = ld_stream(colp + p0 + lg, pol_first); v0 = ld_stream(valp + p0 + lg, pol_first); }
-    if ((u32)(G + lg) < L) { c1 = ld_stream(colp + p0 + G + lg, pol_first); v1 = ld_stream(valp + p0 + G + lg, pol_first); }
     VecT<VEC> xv[U][NT];
 #pragma unroll
     for (int u = 0; u < U; ++u) {
@@ -390,15 +412,13 @@ spmm_chunk_kernel(const SpmmArgs a) {
   const u64 chunk = a.chunk_begin + warp * NGW + lane / G;
   const bool active = chunk < a.chunk_end;
   u64 r0 = 0, j0 = 0, r1 = 0, j1 = 0;
-  bool has_carry = false;
   if (active) {
     r0 = a.chunk_row[chunk]; j0 = a.chunk_nnz[chunk];
     r1 = a.chunk_row[chunk + 1]; j1 = a.chunk_nnz[chunk + 1];
-    has_carry = (r1 < a.m) && (j1 > (u64)__ldg(a.row_ptr + r1));
   }
   const int ldx = D_CT ? D_CT : a.ldx;
   float* carry_row = (a.carry_out && active) ? a.carry_out + (size_t)chunk * (size_t)ldx : nullptr;
-  process_piece<D_CT, G, VEC, NT, RAGGED>(a, active, r0, j0, r1, j1, has_carry, carry_row, lane,
+  process_piece<D_CT, G, VEC, NT, RAGGED>(a, active, r0, j0, r1, j1, carry_row, lane,
                                           scratch[w]);
 }
 
@@ -422,71 +442,135 @@ spmm_dynamic_kernel(const SpmmArgs a) {
     const u64 share = (hi - v + NGW - 1) / NGW;
     const u64 b = min(v + (u64)g * share, hi), e = min(b + share, hi);
     const u64 j0 = __ldg(a.row_ptr + b), j1 = __ldg(a.row_ptr + e);
-    process_piece<D_CT, G, VEC, NT, RAGGED>(a, b < e, b, j0, e, j1, false, nullptr, lane,
+    process_piece<D_CT, G, VEC, NT, RAGGED>(a, b < e, b, j0, e, j1, nullptr, lane,
                                             scratch[w]);
   }
 }
 
-// Adds the partial sums of rows cut by chunk boundaries, in CSR order of the pieces:
-// Y[r] = carry_out[u0] + ... + carry_out[t] + (tail already stored in Y[r]).
-// A warp inspects kFixupPerWarp consecutive chunk boundaries (one per lane; few per warp, so
-// that many chains are resolved concurrently across warps); for every boundary that closes a
-// chain of carries the whole warp sums that chain, lane c handling columns c, c+32, ... of
-// the slab.
-constexpr int kFixupPerWarp = 8;
-__global__ void __launch_bounds__(256)
-carry_fixup_kernel(const u64* __restrict__ row_ptr, const u64* __restrict__ chunk_row,
-                   const u64* __restrict__ chunk_nnz, u64 n_chunks, u64 t_begin, u64 t_end, u64 m,
-                   const float* __restrict__ carry_out, float* __restrict__ y, int ldx, int c0,
-                   int dw) {
-  const int lane = threadIdx.x & 31;
-  const u64 warp = ((u64)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
-  // chunk whose END boundary this lane inspects; boundaries t+1 for t in [t_begin, t_end)
-  const u64 t = t_begin + warp * kFixupPerWarp + lane;
-  bool closes = false;
-  u64 r = 0, u0 = 0;
-  if (lane < kFixupPerWarp && t < t_end && t + 1 < n_chunks) {  // the last chunk ends at (m, nnz)
-    r = chunk_row[t + 1];
+// Carry fix-up. A row cut by chunk boundaries is summed from the partials of the chunks that
+// hold its pieces, in CSR order: y[r] (the row's tail, stored by the chunk in which the row
+// ends) += carry[first] + carry[first+1] + ... + carry[last]. Which boundaries close such a
+// chain, and where the chain starts, depends only on the plan: chain_first_kernel records it
+// once per plan (kNoChain where boundary t+1 closes nothing), so that the fix-up itself is one
+// coalesced load per boundary followed by the chain's loads.
+constexpr u32 kNoChain = 0xffffffffu;
+
+// first[t], t in [0, n_chunks - 1): boundary t+1 (between chunks t and t+1) lies inside row
+// r = chunk_row[t+1] and chunk t+1 ends that row -> the chunk holding the row's first nonzero.
+// Boundaries that close a chain of more than kLongChain partials are also appended to
+// long_list (in no particular order; the chains are independent of each other).
+constexpr u32 kLongChain = 16;
+
+__global__ void chain_first_kernel(const u64* __restrict__ row_ptr, const u64* __restrict__ chunk_row,
+                                   const u64* __restrict__ chunk_nnz, u64 n_chunks, u64 m,
+                                   u32* __restrict__ first, u32* __restrict__ long_list,
+                                   u32* __restrict__ long_count) {
+  const u64 t = (u64)blockIdx.x * blockDim.x + threadIdx.x;
+  if (t >= n_chunks) return;
+  u32 out = kNoChain;
+  if (t + 1 < n_chunks) {  // the last chunk ends at (m, nnz)
+    const u64 r = chunk_row[t + 1];
     if (r < m) {
       const u64 rp = __ldg(row_ptr + r);
-      // boundary t+1 lies inside row r, and chunk t+1 does not carry the same row on
       if (chunk_nnz[t + 1] > rp && chunk_row[t + 2] != r) {
-        closes = true;
-        // the chain starts in the chunk that holds the row's first nonzero: the last chunk u
-        // with chunk_nnz[u] <= rp (binary search instead of walking the chain backwards)
-        u64 lo = 0, hi = t;
+        u64 lo = 0, hi = t;  // last chunk u with chunk_nnz[u] <= rp
         while (lo < hi) {
           const u64 mid = lo + (hi - lo + 1) / 2;
           if (chunk_nnz[mid] <= rp) lo = mid; else hi = mid - 1;
         }
-        u0 = lo;
+        out = (u32)lo;
+        if (t - lo + 1 > kLongChain) long_list[atomicAdd(long_count, 1u)] = (u32)t;
       }
     }
   }
-  unsigned todo = __ballot_sync(kFullMask, closes);
-  while (todo) {
-    const int src = __ffs(todo) - 1;
-    todo &= todo - 1;
-    const u64 rr = __shfl_sync(kFullMask, r, src);
-    const u64 first = __shfl_sync(kFullMask, u0, src);
-    const u64 last = t_begin + warp * kFixupPerWarp + src;
-    for (int c = lane; c < dw; c += 32) {
-      const float* __restrict__ src_c = carry_out + c0 + c;
-      float* dst = y + (size_t)rr * ldx + c0 + c;
-      const float tail = *dst;
-      float s = src_c[(size_t)first * ldx];
-      u64 u = first + 1;
-      // the adds stay in CSR order; the loads of a batch are independent and overlap
-      for (; u + 16 <= last + 1; u += 16) {
-        float part[16];
+  first[t] = out;
+}
+
+// Sum of the partials carry[ub .. ue) of one column vector, in order; the loads of a batch are
+// independent and overlap.
+template <int VEC>
+__device__ __forceinline__ VecT<VEC> chain_sum(const float* __restrict__ src_c, int ldx, u64 ub, u64 ue) {
+  constexpr int kBatch = 8;
+  VecT<VEC> s;
 #pragma unroll
-        for (int q = 0; q < 16; ++q) part[q] = __ldcs(src_c + (size_t)(u + q) * ldx);
+  for (int e = 0; e < VEC; ++e) s.v[e] = 0.0f;
+  u64 u = ub;
+  for (; u + kBatch <= ue; u += kBatch) {
+    VecT<VEC> part[kBatch];
 #pragma unroll
-        for (int q = 0; q < 16; ++q) s += part[q];
+    for (int q = 0; q < kBatch; ++q)
+      part[q] = *reinterpret_cast<const VecT<VEC>*>(src_c + (size_t)(u + q) * ldx);
+#pragma unroll
+    for (int q = 0; q < kBatch; ++q)
+#pragma unroll
+      for (int e = 0; e < VEC; ++e) s.v[e] += part[q].v[e];
+  }
+  for (; u < ue; ++u) {
+    const VecT<VEC> part = *reinterpret_cast<const VecT<VEC>*>(src_c + (size_t)u * ldx);
+#pragma unroll
+    for (int e = 0; e < VEC; ++e) s.v[e] += part.v[e];
+  }
+  return s;
+}
+
+// The first n_long CTAs take one long chain each (more than kLongChain partials): the chain is
+// cut into blockDim/lpc consecutive segments, one per group of lpc lanes, each summed in CSR
+// order; the segment sums are then added in order. The other CTAs give one group of `lpc`
+// lanes (a power of two, <= 32) to every chunk boundary: lane lg sums columns lg*VEC .. of
+// the short chain closed by that boundary, if any, in CSR order. Both orders are fixed by the
+// plan, so the result is deterministic.
+constexpr int kFixupThreads = 256;
+
+template <int VEC>
+__global__ void __launch_bounds__(kFixupThreads)
+carry_fixup_kernel(const u32* __restrict__ chain_first, const u64* __restrict__ chunk_row,
+                   const u32* __restrict__ long_list, u32 n_long, u64 t_begin, u64 t_end,
+                   const float* __restrict__ carry_out, float* __restrict__ y, int ldx, int c0,
+                   int dw, int lpc) {
+  if (blockIdx.x < n_long) {
+    __shared__ VecT<VEC> seg_sum[kFixupThreads];
+    const u64 last = long_list[blockIdx.x];
+    if (last < t_begin || last >= t_end) return;  // CTA-uniform
+    const u64 first = __ldg(chain_first + last), rr = __ldg(chunk_row + last + 1);
+    const int nseg = kFixupThreads / lpc, seg = threadIdx.x / lpc, lg = threadIdx.x % lpc;
+    const u64 per = (last - first + nseg) / nseg;  // ceil(len / nseg)
+    const u64 ub = min(first + (u64)seg * per, last + 1), ue = min(ub + per, last + 1);
+    for (int cb = 0; cb < dw; cb += lpc * VEC) {  // CTA-uniform trip count
+      const int c = cb + lg * VEC;
+      if (c < dw) seg_sum[threadIdx.x] = chain_sum<VEC>(carry_out + c0 + c, ldx, ub, ue);
+      __syncthreads();
+      if (seg == 0 && c < dw) {
+        float* dst = y + (size_t)rr * ldx + c0 + c;
+        VecT<VEC> s = seg_sum[lg];
+        for (int q = 1; q < nseg; ++q) {
+          const VecT<VEC> part = seg_sum[q * lpc + lg];
+#pragma unroll
+          for (int e = 0; e < VEC; ++e) s.v[e] += part.v[e];
+        }
+        const VecT<VEC> tail = *reinterpret_cast<const VecT<VEC>*>(dst);
+#pragma unroll
+        for (int e = 0; e < VEC; ++e) s.v[e] += tail.v[e];
+        *reinterpret_cast<VecT<VEC>*>(dst) = s;
       }
-      for (; u <= last; ++u) s += src_c[(size_t)u * ldx];
-      *dst = s + tail;
+      __syncthreads();
     }
+    return;
+  }
+  const u64 tid = (u64)(blockIdx.x - n_long) * kFixupThreads + threadIdx.x;
+  // chunk whose END boundary this group inspects; boundaries t+1 for t in [t_begin, t_end)
+  const u64 last = t_begin + tid / (unsigned)lpc;
+  const int lg = (int)(tid % (unsigned)lpc);
+  if (last >= t_end) return;
+  const u32 u0 = __ldg(chain_first + last);
+  if (u0 == kNoChain || last - u0 + 1 > kLongChain) return;
+  const u64 rr = __ldg(chunk_row + last + 1);
+  for (int c = lg * VEC; c < dw; c += lpc * VEC) {
+    float* dst = y + (size_t)rr * ldx + c0 + c;
+    const VecT<VEC> tail = *reinterpret_cast<const VecT<VEC>*>(dst);
+    VecT<VEC> s = chain_sum<VEC>(carry_out + c0 + c, ldx, u0, last + 1);
+#pragma unroll
+    for (int e = 0; e < VEC; ++e) s.v[e] += tail.v[e];
+    *reinterpret_cast<VecT<VEC>*>(dst) = s;
   }
 }
 
