@@ -93,7 +93,7 @@ struct spmx_ctx {
   int sm_count = 0;
   cudaEvent_t ev0 = nullptr, ev1 = nullptr;
   int* d_err = nullptr;  // device-side error flag for validation
-  cudaStream_t s_compute = nullptr, s_d2h = nullptr;  // spmx_spmm_host pipeline (lazy)
+  cudaStream_t s_compute = nullptr, s_d2h = nullptr, s_x = nullptr;  // spmx_spmm_host pipeline (lazy)
   std::vector<cudaEvent_t> pipe_events;                // created once, reused by every call
   // grow-only staging used by spmx_spmm_host
   void* ws[5] = {nullptr, nullptr, nullptr, nullptr, nullptr};
@@ -604,6 +604,7 @@ int spmx_ctx_destroy(spmx_ctx* ctx) {
     for (cudaEvent_t e : ctx->pipe_events) cudaEventDestroy(e);
     if (ctx->s_compute) cudaStreamDestroy(ctx->s_compute);
     if (ctx->s_d2h) cudaStreamDestroy(ctx->s_d2h);
+    if (ctx->s_x) cudaStreamDestroy(ctx->s_x);
     cudaEventDestroy(ctx->ev0);
     cudaEventDestroy(ctx->ev1);
     if (ctx->own_stream) cudaStreamDestroy(ctx->stream);
@@ -890,12 +891,13 @@ int spmx_spmm_host(spmx_ctx* ctx, int64_t m, int64_t n, int64_t nnz, const uint6
                    const uint32_t* col, const float* vals, const float* x, int64_t x_rows,
                    int64_t d, float* y, int strategy, unsigned parts, int dynamic, uint64_t batch,
                    unsigned flags, double* times_ms) {
-  // Pipeline over three streams (the transfers dominate: PCIe moves ~8 B per nonzero up and
+  // Pipeline over four streams (the transfers dominate: PCIe moves ~8 B per nonzero up and
   // 4*d B per row down, the kernel needs a fraction of that time):
-  //   stream 0  H2D row_ptr -> validate + plan (the plan needs row_ptr only) -> H2D X
+  //   stream 0  H2D row_ptr -> validate + plan (the plan needs row_ptr only) -> wait for X
   //             -> H2D col/vals of row block 0, 1, ...
   //   stream 1  per block: validate columns, SpMM over the block's chunks, carry fix-up
   //   stream 2  per block: D2H of the Y rows that end in the block
+  //   stream 3  H2D X (while the plan is built on stream 0)
   // Blocks are runs of whole chunks of the work list, so every Y row is final when its
   // block's kernels have run. Dynamic-dispatch plans have no work list: one block.
   return guarded([&] {
@@ -908,8 +910,9 @@ int spmx_spmm_host(spmx_ctx* ctx, int64_t m, int64_t n, int64_t nnz, const uint6
     if (!ctx->s_compute) {
       CUDA_CHECK(cudaStreamCreateWithFlags(&ctx->s_compute, cudaStreamNonBlocking));
       CUDA_CHECK(cudaStreamCreateWithFlags(&ctx->s_d2h, cudaStreamNonBlocking));
+      CUDA_CHECK(cudaStreamCreateWithFlags(&ctx->s_x, cudaStreamNonBlocking));
     }
-    cudaStream_t s0 = ctx->stream, s1 = ctx->s_compute, s2 = ctx->s_d2h;
+    cudaStream_t s0 = ctx->stream, s1 = ctx->s_compute, s2 = ctx->s_d2h, s3 = ctx->s_x;
     constexpr int kMaxBlocks = 8;
     cudaEvent_t ev_t[4];            // timing marks on stream 0 / 2
     cudaEvent_t ev_x, ev_in[kMaxBlocks], ev_done[kMaxBlocks];
@@ -948,7 +951,10 @@ int spmx_spmm_host(spmx_ctx* ctx, int64_t m, int64_t n, int64_t nnz, const uint6
       const auto t_host0 = std::chrono::steady_clock::now();
       CUDA_CHECK(cudaEventRecord(ev_t[0], s0));
       CUDA_CHECK(cudaMemcpyAsync(d_rp, row_ptr, ((size_t)m + 1) * 8, cudaMemcpyHostToDevice, s0));
-      // X starts moving while the plan is being built from row_ptr
+      // X moves on its own stream while the plan is being built from row_ptr
+      CUDA_CHECK(cudaStreamWaitEvent(s3, ev_t[0], 0));
+      CUDA_CHECK(cudaMemcpyAsync(d_x, x, (size_t)n * (size_t)d * 4, cudaMemcpyHostToDevice, s3));
+      CUDA_CHECK(cudaEventRecord(ev_x, s3));
       CUDA_CHECK(cudaMemsetAsync(ctx->d_err, 0, sizeof(int), s0));
       spmx_dev::validate_row_ptr_kernel<<<validate_grid(ctx, (u64)m), 256, 0, s0>>>(
           d_rp, (u64)m, (u64)nnz, ctx->d_err);
@@ -957,14 +963,11 @@ int spmx_spmm_host(spmx_ctx* ctx, int64_t m, int64_t n, int64_t nnz, const uint6
       CUDA_CHECK(cudaMemcpyAsync(&err, ctx->d_err, sizeof(int), cudaMemcpyDeviceToHost, s0));
       CUDA_CHECK(cudaStreamSynchronize(s0));
       if (err) throw InvalidArg(std::string("invalid CSR: ") + csr_error_text(err));
-      // plan first (a fraction of a millisecond; its cudaMalloc/cudaFree calls would otherwise
-      // serialise against transfers in flight), then everything else streams
+      // the plan (a fraction of a millisecond, stream-ordered allocations only) overlaps the
+      // X upload; col/vals follow X so that they do not take bandwidth from it
       plan = plan_build(ctx, &a, strategy, parts, dynamic, batch, flags);  // syncs stream 0
       ensure_carry(plan, d);
       const auto t_host1 = std::chrono::steady_clock::now();
-      CUDA_CHECK(cudaMemcpyAsync(d_x, x, (size_t)n * (size_t)d * 4, cudaMemcpyHostToDevice, s0));
-      CUDA_CHECK(cudaEventRecord(ev_x, s0));
-      CUDA_CHECK(cudaEventRecord(ev_t[1], s0));
 
       // blocks = runs of whole chunks with about equal nonzero counts
       int nblocks = 1;
@@ -983,6 +986,8 @@ int spmx_spmm_host(spmx_ctx* ctx, int64_t m, int64_t n, int64_t nnz, const uint6
         // a block's first chunk may start inside a row whose head is in the previous block; the
         // nonzeros it needs still start at its own chunk_nnz, which is what nnz_b holds
       }
+      CUDA_CHECK(cudaStreamWaitEvent(s0, ev_x, 0));
+      CUDA_CHECK(cudaEventRecord(ev_t[1], s0));
       for (int b = 0; b < nblocks; ++b) {
         const u64 n0 = nnz_b[b], n1 = nnz_b[b + 1];
         if (n1 > n0) {
@@ -1030,6 +1035,7 @@ int spmx_spmm_host(spmx_ctx* ctx, int64_t m, int64_t n, int64_t nnz, const uint6
       cudaStreamSynchronize(s0);
       cudaStreamSynchronize(s1);
       cudaStreamSynchronize(s2);
+      cudaStreamSynchronize(s3);
       cleanup();
       throw;
     }
