@@ -426,24 +426,45 @@ spmm_chunk_kernel(const SpmmArgs a) {
 // from a device counter — next_batch(), src/partition.cpp:29-33; the JIT'd `lock xadd`
 // driver, src/jit.cpp:106-121. One claim per warp keeps the claimed ranges disjoint and
 // covering [0, m) exactly as the reference's dispatcher does; the claimed rows are dealt
-// to the warp's groups in equal contiguous shares (rows are never split).
+// to the warp's groups in contiguous runs of about equal nonzero count (rows are never split).
 template <int D_CT, int G, int VEC, int NT, bool RAGGED>
 __global__ void __launch_bounds__(kWarpsPerCta * 32, Tune<D_CT, NT>::kMinCtas)
 spmm_dynamic_kernel(const SpmmArgs a) {
   constexpr int NGW = 32 / G;
   __shared__ WarpScratch<G> scratch[kWarpsPerCta];
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5, g = lane / G;
-  for (;;) {
-    u64 v = 0;
-    if (lane == 0) v = atomicAdd(a.counter, a.batch);
-    v = __shfl_sync(kFullMask, v, 0);
-    if (v >= a.m) return;
+  u64 v = 0;
+  if (lane == 0) v = atomicAdd(a.counter, a.batch);
+  v = __shfl_sync(kFullMask, v, 0);
+  while (v < a.m) {
+    // the next claim is issued now, so that its round trip overlaps this batch's work (a warp
+    // over-claims once at the end, which next_batch() answers with "nothing left" as well)
+    u64 vnext = 0;
+    if (lane == 0) vnext = atomicAdd(a.counter, a.batch);
     const u64 hi = min(v + a.batch, a.m);
-    const u64 share = (hi - v + NGW - 1) / NGW;
-    const u64 b = min(v + (u64)g * share, hi), e = min(b + share, hi);
+    // the claimed rows are dealt to the groups in contiguous runs of about equal nonzero count
+    const u64 jl = __ldg(a.row_ptr + v), jh = __ldg(a.row_ptr + hi);
+    u64 bnd[2];
+#pragma unroll
+    for (int s = 0; s < 2; ++s) {
+      const int q = g + s;
+      u64 r = q == 0 ? v : hi;
+      if (q > 0 && q < NGW) {
+        const u64 target = jl + (jh - jl) * (u64)q / NGW;
+        u64 lo = v, up = hi;  // first row in [v, hi] whose start is >= target
+        while (lo < up) {
+          const u64 mid = lo + (up - lo) / 2;
+          if (__ldg(a.row_ptr + mid) < target) lo = mid + 1; else up = mid;
+        }
+        r = lo;
+      }
+      bnd[s] = r;
+    }
+    const u64 b = bnd[0], e = bnd[1];
     const u64 j0 = __ldg(a.row_ptr + b), j1 = __ldg(a.row_ptr + e);
     process_piece<D_CT, G, VEC, NT, RAGGED>(a, b < e, b, j0, e, j1, nullptr, lane,
                                             scratch[w]);
+    v = __shfl_sync(kFullMask, vnext, 0);
   }
 }
 
