@@ -339,7 +339,9 @@ __device__ __forceinline__ void process_piece(const SpmmArgs& a, bool active, u6
     const u32 Lmax = __reduce_max_sync(kFullMask, L);
     if (Lmax == 0) continue;  // warp-uniform
     int k = 0;  // current row = k-th non-empty row of the window
-    u32 left = (L > 0) ? s_end[0] - p0 : 0x7fffffffu;  // nonzeros left in the current row
+    // position (relative to the current batch) of the last nonzero of the current row
+    constexpr int kNoRowEnd = 0x3fffffff;
+    int e_rel = (L > 0) ? (int)min(s_end[0] - p0 - 1u, (u32)kNoRowEnd) : kNoRowEnd;
 
     // ---- walk the window's nonzeros ---------------------------------------------------------
     VecT<VEC> xv[U][NT];
@@ -355,6 +357,7 @@ __device__ __forceinline__ void process_piece(const SpmmArgs& a, bool active, u6
     }
 #pragma unroll 1
     for (u32 nb = 0; nb < Lmax; nb += G) {
+      const int rem = (int)min(L > nb ? L - nb : 0u, 0x7fffffffu);  // positions this group has left
       u32 c2 = 0;
       float v2 = 0.0f;
       if (nb + 2 * G + lg < L) {
@@ -368,7 +371,7 @@ __device__ __forceinline__ void process_piece(const SpmmArgs& a, bool active, u6
         const float vq = __shfl_sync(kFullMask, v0, t, G);
         const u32 kq = (t + U < G) ? __shfl_sync(kFullMask, c0, t + U, G)
                                    : __shfl_sync(kFullMask, c1, t + U - G, G);
-        if (nb + t < L) {
+        if (t < rem) {
 #pragma unroll
           for (int tt = 0; tt < NT; ++tt)
             if (!RAGGED || (tt * G + lg) * VEC < a.dw) {
@@ -377,15 +380,15 @@ __device__ __forceinline__ void process_piece(const SpmmArgs& a, bool active, u6
                 acc[tt][e] = __fmaf_rn(vq, xv[u][tt].v[e], acc[tt][e]);
             }
         }
-        if (--left == 0) {  // row k ends here: store it, start the next one
+        if (t == e_rel) {  // row k ends here: store it, start the next one
           const u64 rr = wbase + s_idx[k];
           float* dst = (rr < r1) ? a.y + (size_t)rr * (size_t)ldx : carry_row;
           store_row<G, VEC, NT, RAGGED>(a, dst, lg, acc, pol_first);
           zero_acc(acc);
           ++k;
-          left = (k < count) ? s_end[k] - s_end[k - 1] : 0x7fffffffu;
+          e_rel = (k < count) ? (int)min((u32)e_rel + (s_end[k] - s_end[k - 1]), (u32)kNoRowEnd) : kNoRowEnd;
         }
-        if (nb + t + U < L) {
+        if (t + U < rem) {
           const float* xr = xbase + (size_t)kq * (size_t)ldx;
 #pragma unroll
           for (int tt = 0; tt < NT; ++tt)
@@ -394,6 +397,7 @@ __device__ __forceinline__ void process_piece(const SpmmArgs& a, bool active, u6
       }
       c0 = c1; v0 = v1;
       c1 = c2; v1 = v2;
+      if (e_rel < kNoRowEnd) e_rel -= G;
     }
     ws = we;
   }
