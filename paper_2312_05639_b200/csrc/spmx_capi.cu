@@ -123,6 +123,7 @@ struct spmx_plan {
   u64* ranges = nullptr;     // 2*parts, device (absent under dynamic dispatch)
   u64* chunk_row = nullptr;  // n_chunks+1
   u64* chunk_nnz = nullptr;  // n_chunks+1
+  spmx_dev::WorkItem* work = nullptr;  // n_chunks: the chunks in launch order (sorted inside tiles)
   uint32_t* chain_first = nullptr;  // n_chunks: start of the carry chain closed by boundary t+1
   uint32_t* long_buf = nullptr;     // [count | boundaries closing chains longer than kLongChain]
   uint32_t* long_list = nullptr;    // = long_buf + 1
@@ -343,6 +344,7 @@ void launch_fixup(const spmx_plan* p, u64 tb, u64 te, float* d_y, int ldx, int c
 void run_kernels(spmx_ctx* ctx, const spmx_plan* p, const spmx_csr* a, const float* d_x,
                  int64_t d, float* d_y, cudaStream_t st, u64 cb, u64 ce, const int* abort_flag) {
   if (a->m == 0) return;
+  if (!p->dynamic && ce <= cb) return;  // empty block of the host pipeline
   const bool aligned16 = ((uintptr_t)d_x % 16 == 0) && ((uintptr_t)d_y % 16 == 0);
   const int vec = (d % 4 == 0 && aligned16) ? 4 : 1;
   const int slab_max = 32 * vec * 8;  // G=32, NT=8
@@ -356,8 +358,7 @@ void run_kernels(spmx_ctx* ctx, const spmx_plan* p, const spmx_csr* a, const flo
   args.x = d_x;
   args.y = d_y;
   args.carry_out = p->may_carry ? p->carry : nullptr;
-  args.chunk_row = p->chunk_row;
-  args.chunk_nnz = p->chunk_nnz;
+  args.work = p->work;
   args.n_chunks = p->n_chunks;
   args.chunk_begin = cb;
   args.chunk_end = ce;
@@ -428,6 +429,7 @@ void plan_free(spmx_plan* p) {
   if (!p) return;
   dev_free_async(p->ctx, p->ranges);
   dev_free_async(p->ctx, p->chunk_row);
+  dev_free_async(p->ctx, p->work);
   dev_free_async(p->ctx, p->chain_first);
   dev_free_async(p->ctx, p->long_buf);
   dev_free_async(p->ctx, p->chunk_nnz);
@@ -532,6 +534,13 @@ spmx_plan* plan_build(spmx_ctx* ctx, const spmx_csr* a, int strategy, unsigned p
       dev_free_async(ctx, d_cnt);
       dev_free_async(ctx, d_off);
       p->may_carry = true;
+    }
+    if (p->n_chunks > 0) {
+      p->work = dev_alloc_async<spmx_dev::WorkItem>(ctx, (size_t)p->n_chunks);
+      spmx_dev::work_items_kernel<spmx_dev::WorkItem>
+          <<<blocks_for(p->n_chunks, spmx_dev::kSortTile), spmx_dev::kSortTile, 0, ctx->stream>>>(
+              p->chunk_row, p->chunk_nnz, p->n_chunks, p->work);
+      post_launch();
     }
     CUDA_CHECK(cudaStreamSynchronize(ctx->stream));
     dev_free_async(ctx, d_diag);
@@ -977,7 +986,10 @@ int spmx_spmm_host(spmx_ctx* ctx, int64_t m, int64_t n, int64_t nnz, const uint6
         cb.assign(nblocks + 1, 0);
         row_b.assign(nblocks + 1, 0);
         nnz_b.assign(nblocks + 1, 0);
-        for (int b = 0; b <= nblocks; ++b) cb[b] = plan->n_chunks * (u64)b / (u64)nblocks;
+        // whole sort tiles, so that a block's launch slots hold exactly the block's chunks
+        for (int b = 0; b < nblocks; ++b)
+          cb[b] = plan->n_chunks * (u64)b / (u64)nblocks / spmx_dev::kSortTile * spmx_dev::kSortTile;
+        cb[nblocks] = plan->n_chunks;
         for (int b = 0; b <= nblocks; ++b) {
           CUDA_CHECK(cudaMemcpyAsync(&row_b[b], plan->chunk_row + cb[b], 8, cudaMemcpyDeviceToHost, s0));
           CUDA_CHECK(cudaMemcpyAsync(&nnz_b[b], plan->chunk_nnz + cb[b], 8, cudaMemcpyDeviceToHost, s0));

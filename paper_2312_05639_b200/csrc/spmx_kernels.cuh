@@ -149,6 +149,14 @@ __device__ __forceinline__ void st_y(float* p, const float* a, u64 pol) {
 #endif
 }
 
+// One entry of the launch-order work list: chunk `chunk` of the plan, i.e. the piece of the
+// merge path between (r0, j0) and (r1, j1).
+struct alignas(16) WorkItem {
+  u64 r0, j0, r1, j1;
+  u64 chunk;
+  u64 pad_;
+};
+
 struct SpmmArgs {
   const u64* __restrict__ row_ptr;
   const u32* __restrict__ col;
@@ -156,8 +164,7 @@ struct SpmmArgs {
   const float* __restrict__ x;   // N x ldx
   float* __restrict__ y;         // M x ldx
   float* __restrict__ carry_out; // n_chunks x ldx (rows cut by a chunk end), may be null in exact mode
-  const u64* __restrict__ chunk_row;  // n_chunks + 1
-  const u64* __restrict__ chunk_nnz;  // n_chunks + 1
+  const WorkItem* __restrict__ work;  // n_chunks work items in launch order (see work_items_kernel)
   u64 n_chunks;     // size of the whole work list
   u64 chunk_begin;  // this launch processes chunks [chunk_begin, chunk_end)
   u64 chunk_end;
@@ -413,12 +420,12 @@ spmm_chunk_kernel(const SpmmArgs a) {
   const u64 warp = (u64)blockIdx.x * kWarpsPerCta + w;
   if (a.chunk_begin + warp * NGW >= a.chunk_end) return;  // whole warp idle
   if (a.abort_flag && *(volatile const int*)a.abort_flag) return;
-  const u64 chunk = a.chunk_begin + warp * NGW + lane / G;
-  const bool active = chunk < a.chunk_end;
-  u64 r0 = 0, j0 = 0, r1 = 0, j1 = 0;
+  const u64 slot = a.chunk_begin + warp * NGW + lane / G;
+  const bool active = slot < a.chunk_end;
+  u64 r0 = 0, j0 = 0, r1 = 0, j1 = 0, chunk = 0;
   if (active) {
-    r0 = a.chunk_row[chunk]; j0 = a.chunk_nnz[chunk];
-    r1 = a.chunk_row[chunk + 1]; j1 = a.chunk_nnz[chunk + 1];
+    const WorkItem it = a.work[slot];
+    r0 = it.r0; j0 = it.j0; r1 = it.r1; j1 = it.j1; chunk = it.chunk;
   }
   const int ldx = D_CT ? D_CT : a.ldx;
   float* carry_row = (a.carry_out && active) ? a.carry_out + (size_t)chunk * (size_t)ldx : nullptr;

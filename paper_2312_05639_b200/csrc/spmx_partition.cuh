@@ -189,6 +189,54 @@ __global__ void chunk_coords_kernel(const u64* __restrict__ row_ptr, u64 m, u64 
   out_nnz[c] = j;
 }
 
+// Launch-order work list. The lane groups of a warp run their pieces in lockstep, so a warp
+// is as slow as its longest piece: within tiles of kSortTile consecutive chunks the chunks are
+// ordered by nonzero count (ties by chunk index: deterministic), so that the 32/G pieces a
+// warp takes are of nearly equal length. Tiles keep the order local (X and Y locality, and
+// the host pipeline's row blocks are runs of whole tiles). One CTA of kSortTile threads per
+// tile, bitonic sort in shared memory.
+#ifndef SPMX_SORT_TILE
+#define SPMX_SORT_TILE 256
+#endif
+constexpr int kSortTile = SPMX_SORT_TILE;
+
+template <typename Item>
+__global__ void __launch_bounds__(kSortTile)
+work_items_kernel(const u64* __restrict__ chunk_row, const u64* __restrict__ chunk_nnz,
+                  u64 n_chunks, Item* __restrict__ work) {
+  __shared__ u64 key[kSortTile];
+  const u64 base = (u64)blockIdx.x * kSortTile;
+  const u64 c = base + threadIdx.x;
+  u64 k = ~0ull;  // padding sorts last
+  if (c < n_chunks) {
+    const u64 span = chunk_nnz[c + 1] - chunk_nnz[c];
+    k = (min(span, 0xffffffffull) << 32) | threadIdx.x;
+  }
+  key[threadIdx.x] = k;
+  __syncthreads();
+  for (int size = 2; size <= kSortTile; size <<= 1) {
+    for (int stride = size >> 1; stride > 0; stride >>= 1) {
+      const int i = threadIdx.x, j = i ^ stride;
+      if (j > i) {
+        const u64 a = key[i], b = key[j];
+        const bool up = (i & size) == 0;
+        if ((a > b) == up) { key[i] = b; key[j] = a; }
+      }
+      __syncthreads();
+    }
+  }
+  const u64 slot = base + threadIdx.x;
+  if (slot < n_chunks) {
+    const u64 src = base + (key[threadIdx.x] & 0xffffffffull);
+    Item it;
+    it.r0 = chunk_row[src]; it.j0 = chunk_nnz[src];
+    it.r1 = chunk_row[src + 1]; it.j1 = chunk_nnz[src + 1];
+    it.chunk = src;
+    it.pad_ = 0;
+    work[slot] = it;
+  }
+}
+
 // validate_csr, src/csr.cpp:18-42, on the device. err receives the largest code seen:
 // 2 row_ptr[0] != 0, 3 row_ptr[m] != nnz, 4 row_ptr decreasing, 5 column out of range.
 __global__ void validate_row_ptr_kernel(const u64* __restrict__ row_ptr, u64 m, u64 nnz, int* err) {
