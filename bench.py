@@ -245,6 +245,7 @@ def main():
     else:
         a = a_full
         nnz_total, m_total = a.nnz, a.m
+    torch.cuda.empty_cache()  # hand the generator's scratch back: the library allocates with cudaMalloc
     da = ctx.csr_wrap(a)
     y = torch.empty(a.m, d, device=dev)
     plan = ctx.plan(da, args.strategy, 0, flags=flags)
@@ -329,6 +330,7 @@ def main():
     rp_n, col_n = rp_h.numpy().view(np.uint64), col_h.numpy().view(np.uint32)
     vals_n, x_n, y_n = vals_h.numpy(), x_h.numpy(), y_h.numpy()
     e2e_steps = max(3, min(args.steps, 10))
+    torch.cuda.empty_cache()
     ectx = Context(local_rank)  # private stream
 
     def e2e_once():
