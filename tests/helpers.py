@@ -52,3 +52,19 @@ def split_row_mask(m, chunk_row, chunk_nnz, row_ptr):
         if r < m and int(j) > int(row_ptr[r]):
             mask[r] = True
     return mask
+
+
+def chain_lengths(m, chunk_row, chunk_nnz, row_ptr):
+    """Lengths of the carry chains of a plan: for every chunk boundary that lies inside a row
+    which the next chunk ends, the number of chunks holding partial sums of that row before
+    the boundary (what carry_fixup_kernel adds to the row's tail)."""
+    cr = np.asarray(chunk_row, np.int64); cj = np.asarray(chunk_nnz, np.int64)
+    rp = np.asarray(row_ptr, np.int64)
+    out = []
+    n = len(cr) - 1
+    for t in range(n - 1):
+        r = cr[t + 1]
+        if r < m and cj[t + 1] > rp[r] and cr[t + 2] != r:
+            first = int(np.searchsorted(cj, rp[r], side="right")) - 1
+            out.append(t - first + 1)
+    return np.asarray(out, np.int64)

@@ -10,7 +10,7 @@ import numpy as np
 import pytest
 import torch
 
-from helpers import D_POOL, north_star_ok, rand_csr, split_row_mask
+from helpers import D_POOL, chain_lengths, north_star_ok, rand_csr, split_row_mask
 
 pytestmark = pytest.mark.gpu
 
@@ -190,7 +190,8 @@ def test_long_rows_and_skew(ctx, oracle):
     nnz = int(rp[-1])
     col = np.concatenate([np.sort(rng.choice(n, size=l, replace=False)) for l in lens]).astype(np.uint32)
     vals = (rng.random(nnz, np.float32) * 2 - 1).astype(np.float32)
-    for d in (32, 64, 128, 45):
+    longest_chain = 0
+    for d in (32, 64, 128, 45, 6):
         x = (rng.random((n, d), np.float32) * 2 - 1).astype(np.float32)
         want = oracle.spmm_fused(m, n, rp, col, vals, x)
         unf = oracle.spmm_unfused(m, n, rp, col, vals, x)
@@ -202,10 +203,15 @@ def test_long_rows_and_skew(ctx, oracle):
                 y, p = run(ctx, m, n, rp, col, vals, x, s, t, 0)
                 assert north_star_ok(y, unf, bound), (d, s, t)
                 cr, cj = p.chunks()
+                ch = chain_lengths(m, cr, cj, rp)
+                longest_chain = max(longest_chain, int(ch.max()) if ch.size else 0)
                 exact_rows = ~split_row_mask(m, cr, cj, rp) & (lens < LONG_SEG)
                 assert np.array_equal(y[exact_rows].view(np.uint32), want[exact_rows].view(np.uint32))
                 y2, _ = run(ctx, m, n, rp, col, vals, x, s, t, 0)
                 assert np.array_equal(y.view(np.uint32), y2.view(np.uint32)), "not deterministic"
+    # both fix-up paths ran: short chains (one lane group each) and long ones (one CTA each,
+    # more than 16 partials; kLongChain in csrc/spmx_kernels.cuh)
+    assert longest_chain > 16
 
 
 def test_config_siblings_match_reference_checksums(ctx, oracle):
