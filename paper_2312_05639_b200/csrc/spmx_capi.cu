@@ -325,18 +325,30 @@ void launch_fixup(const spmx_plan* p, u64 tb, u64 te, float* d_y, int ldx, int c
   while (lpc < 32 && lpc * vec < dw) lpc *= 2;
   constexpr int kT = spmx_dev::kFixupThreads;
   const unsigned grid = p->n_long + blocks_for((te - tb) * (u64)lpc, kT);
+  // Programmatic stream serialisation: the grid may start while the SpMM kernel before it on
+  // the stream is draining; it waits (griddepcontrol.wait) before it reads that kernel's output.
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = dim3(grid);
+  cfg.blockDim = dim3(kT);
+  cfg.stream = st;
+  cudaLaunchAttribute attr{};
+  attr.id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr.val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = &attr;
+  cfg.numAttrs = 1;
+  const uint32_t* cf = p->chain_first;
+  const u64* cr = p->chunk_row;
+  const uint32_t* ll = p->long_list;
+  const float* carry = p->carry;
   if (vec == 4)
-    spmx_dev::carry_fixup_kernel<4><<<grid, kT, 0, st>>>(p->chain_first, p->chunk_row, p->long_list,
-                                                          p->n_long, tb, te, p->carry, d_y, ldx,
-                                                          c0, dw, lpc);
+    CUDA_CHECK(cudaLaunchKernelEx(&cfg, spmx_dev::carry_fixup_kernel<4>, cf, cr, ll, p->n_long, tb, te,
+                                  carry, d_y, ldx, c0, dw, lpc));
   else if (vec == 2)
-    spmx_dev::carry_fixup_kernel<2><<<grid, kT, 0, st>>>(p->chain_first, p->chunk_row, p->long_list,
-                                                          p->n_long, tb, te, p->carry, d_y, ldx,
-                                                          c0, dw, lpc);
+    CUDA_CHECK(cudaLaunchKernelEx(&cfg, spmx_dev::carry_fixup_kernel<2>, cf, cr, ll, p->n_long, tb, te,
+                                  carry, d_y, ldx, c0, dw, lpc));
   else
-    spmx_dev::carry_fixup_kernel<1><<<grid, kT, 0, st>>>(p->chain_first, p->chunk_row, p->long_list,
-                                                          p->n_long, tb, te, p->carry, d_y, ldx,
-                                                          c0, dw, lpc);
+    CUDA_CHECK(cudaLaunchKernelEx(&cfg, spmx_dev::carry_fixup_kernel<1>, cf, cr, ll, p->n_long, tb, te,
+                                  carry, d_y, ldx, c0, dw, lpc));
   post_launch();
 }
 

@@ -418,6 +418,10 @@ spmm_chunk_kernel(const SpmmArgs a) {
   __shared__ WarpScratch<G> scratch[kWarpsPerCta];
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
   const u64 warp = (u64)blockIdx.x * kWarpsPerCta + w;
+  // the fix-up kernel is launched with programmatic stream serialisation: let its CTAs take
+  // the SM slots this grid frees in its tail (they wait for this grid's completion before
+  // they touch the carries)
+  asm volatile("griddepcontrol.launch_dependents;");
   if (a.chunk_begin + warp * NGW >= a.chunk_end) return;  // whole warp idle
   if (a.abort_flag && *(volatile const int*)a.abort_flag) return;
   const u64 slot = a.chunk_begin + warp * NGW + lane / G;
@@ -564,6 +568,7 @@ carry_fixup_kernel(const u32* __restrict__ chain_first, const u64* __restrict__ 
     const u64 last = long_list[blockIdx.x];
     if (last < t_begin || last >= t_end) return;  // CTA-uniform
     const u64 first = __ldg(chain_first + last), rr = __ldg(chunk_row + last + 1);
+    asm volatile("griddepcontrol.wait;" ::: "memory");  // plan data above, SpMM results below
     const int nseg = kFixupThreads / lpc, seg = threadIdx.x / lpc, lg = threadIdx.x % lpc;
     const u64 per = (last - first + nseg) / nseg;  // ceil(len / nseg)
     const u64 ub = min(first + (u64)seg * per, last + 1), ue = min(ub + per, last + 1);
@@ -596,6 +601,7 @@ carry_fixup_kernel(const u32* __restrict__ chain_first, const u64* __restrict__ 
   const u32 u0 = __ldg(chain_first + last);
   if (u0 == kNoChain || last - u0 + 1 > kLongChain) return;
   const u64 rr = __ldg(chunk_row + last + 1);
+  asm volatile("griddepcontrol.wait;" ::: "memory");  // plan data above, SpMM results below
   for (int c = lg * VEC; c < dw; c += lpc * VEC) {
     float* dst = y + (size_t)rr * ldx + c0 + c;
     const VecT<VEC> tail = *reinterpret_cast<const VecT<VEC>*>(dst);
