@@ -418,7 +418,7 @@ void run_kernels(spmx_ctx* ctx, const spmx_plan* p, const spmx_csr* a, const flo
     } else if (vec == 4 && c0 == 0 && d == 64) {
       launch_one<64, 16 / SPMX_NT, 4, SPMX_NT, false>(p, args, st, ctx->sm_count);
     } else if (vec == 4 && c0 == 0 && d == 128) {
-      launch_one<128, 32 / SPMX_NT, 4, SPMX_NT, false>(p, args, st, ctx->sm_count);
+      launch_one<128, 8, 4, 4, false>(p, args, st, ctx->sm_count);  // see Tune<128, 4>
     } else {
       const int lanes = (dw + vec - 1) / vec;
       int g = pow2_ceil(std::min(lanes, 32));

@@ -215,6 +215,13 @@ struct Tune {
   static constexpr int kMinCtas = ((NT <= 2) ? SPMX_MIN_CTAS : 1) * (8 / kWarpsPerCta);
   static constexpr int kInFlight = SPMX_U;
 };
+// d = 128: four float4 tiles per lane, 8 lanes per row (4 rows per warp step instead of 2:
+// fewer instructions per nonzero), same 16 loads in flight and 16 warps/SM.
+template <>
+struct Tune<128, 4> {
+  static constexpr int kMinCtas = SPMX_MIN_CTAS * (8 / kWarpsPerCta);
+  static constexpr int kInFlight = SPMX_U;
+};
 template <>
 struct Tune<32, 1> {
   static constexpr int kMinCtas = 3 * (8 / kWarpsPerCta);
