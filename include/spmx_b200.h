@@ -47,9 +47,11 @@ extern "C" {
                                order: bitwise equal to the reference's run_spmm for all three
                                strategies. Without it (default), ranges heavier
                                than the chunk budget and the merge strategy split rows at nonzero
-                               granularity; split rows are summed from per-chunk partials in CSR
-                               order (deterministic, within the north_star tolerance), all other
-                               rows stay bitwise equal. */
+                               granularity; split rows are summed from per-chunk partials in an
+                               order fixed by the plan (CSR order of the pieces; rows cut into more
+                               than 16 pieces: 16 runs of consecutive pieces, then the runs) —
+                               deterministic, within the north_star tolerance; all other rows stay
+                               bitwise equal. */
 #define SPMX_NO_COOP 2u     /* reserved (no effect) */
 #define SPMX_JIT_WIDTH 4u   /* instantiate the kernel for exactly this d at run time (NVRTC, cached
                                per d and device) instead of using the runtime-d kernels: the GPU

@@ -26,6 +26,7 @@ def main():
     ap.add_argument("--parts", type=int, default=0)
     ap.add_argument("--d", type=int, default=None, help="override the dense width")
     ap.add_argument("--modes", default="fast,exact")
+    ap.add_argument("--strategies", default="row,nnz,merge,row-dyn")
     args = ap.parse_args()
     peak = 6551.0
     try:
@@ -48,7 +49,7 @@ def main():
         da = ctx.csr_wrap(a)
         y = torch.empty(a.m, d, device="cuda")
         ref = None
-        for strat in ("row", "nnz", "merge", "row-dyn"):
+        for strat in args.strategies.split(","):
             for mode in args.modes.split(","):
                 flags = {"fast": 0, "exact": EXACT_ORDER, "nocoop": NO_COOP, "jit": JIT_WIDTH}[mode]
                 dyn = strat == "row-dyn"
