@@ -157,6 +157,8 @@ int spmx_max_relative_error(spmx_ctx* ctx, const float* d_y, const float* d_ref,
 /* run-time code generation counters (RunReport.codegen_s of the reference, executor.cpp:54-60):
  * kernels compiled so far in this process and the seconds spent compiling them */
 int spmx_jit_stats(uint64_t* kernels_compiled, double* seconds);
+/* 1 when the run-time compiler (libnvrtc) can be loaded, i.e. SPMX_JIT_WIDTH can be honoured */
+int spmx_jit_available(void);
 
 /* ---- helpers for the reference's report fields ---------------------------------------------- */
 /* checksum(Y), dense.cpp:17-28, of a device buffer (FNV-1a is sequential: the buffer is copied

@@ -1101,6 +1101,8 @@ int spmx_max_relative_error(spmx_ctx* ctx, const float* d_y, const float* d_ref,
   });
 }
 
+int spmx_jit_available(void) { return spmx_jit::Nvrtc::get().ok() ? 1 : 0; }
+
 int spmx_jit_stats(uint64_t* kernels_compiled, double* seconds) {
   return guarded([&] {
     std::lock_guard<std::mutex> lock(spmx_jit::mu());

@@ -5,15 +5,14 @@
 // CSR order, acc[j] = fma(v, X[k][j], acc[j]) with single rounding
 // (src/interp.cpp:36-51 defines the bitwise result), store the row once.
 //
-// Mapping: a "group" of G lanes owns one output row at a time; each lane holds
-// NT x VEC consecutive-column accumulators (d = 32/64/128 -> G = 8/16/32, VEC = 4,
-// NT = 1: one float4 per lane). A warp holds 32/G groups and owns one "chunk" of
-// the work list (spmx_plan): the contiguous piece of the merge path between two
-// (row, nnz) coordinates. Rows that lie wholly inside a chunk are accumulated by
-// a single group in CSR order (bitwise equal to the reference). A row cut by a
-// chunk boundary leaves a partial in carry_out[chunk], added in CSR order by
-// carry_fixup_kernel. Long row segments are shared by all groups of the warp and
-// combined with warp shuffles.
+// Mapping: a "group" of G lanes owns one "chunk" of the work list (spmx_plan) — the
+// contiguous piece of the merge path between two (row, nnz) coordinates — and one output
+// row at a time; each lane holds NT x VEC consecutive-column accumulators (d = 32 -> G = 8,
+// NT = 1; d = 64 -> G = 8, NT = 2; d = 128 -> G = 8, NT = 4; VEC = 4: float4 tiles). The
+// 32/G groups of a warp run the same instruction stream on different chunks. Rows that lie
+// wholly inside a chunk are accumulated by a single group in CSR order (bitwise equal to
+// the reference). A row cut by a chunk boundary leaves a partial in carry_out[chunk];
+// carry_fixup_kernel adds the partials in an order fixed by the plan.
 //
 // No tensor cores: the path is an irregular gather-reduce (2 flop per 4..8 bytes
 // gathered), bounded by L2->SM / L1 gather bandwidth, not by math.

@@ -212,8 +212,10 @@ struct RunConfig {
   unsigned trials = 1;
   bool collect_counters = false;
   int device = 0;          // extension: which GPU
-  bool jit_width = false;  // extension: compile the kernel for exactly X.cols at run time (NVRTC),
-                           // the counterpart of the reference's per-d code generation
+  bool jit_width = true;   // extension: compile the kernel for exactly X.cols at run time (NVRTC,
+                           // cached per d; d = 32/64/128 are precompiled), the counterpart of the
+                           // reference's per-d code generation behind Backend::Native. Ignored
+                           // when libnvrtc cannot be loaded (the runtime-d kernels run instead).
 };
 
 struct RunReport {
@@ -282,8 +284,9 @@ inline std::pair<DenseMatrix, RunReport> run_spmm(const CsrMatrix& a, const Dens
   if (cfg.dynamic_dispatch && cfg.strategy != Strategy::RowSplit)
     throw std::invalid_argument("dynamic dispatch pairs with row-split only");
   const bool dynamic = cfg.dynamic_dispatch && cfg.strategy == Strategy::RowSplit;
+  const bool jit = cfg.jit_width && spmx_jit_available() != 0;
   const unsigned flags = (cfg.backend == Backend::Interp ? SPMX_EXACT_ORDER : 0u) |
-                         (cfg.jit_width ? SPMX_JIT_WIDTH : 0u);
+                         (jit ? SPMX_JIT_WIDTH : 0u);
 
   detail::Ctx c(cfg.device);
   detail::DevCsr da(c, a);
@@ -308,7 +311,7 @@ inline std::pair<DenseMatrix, RunReport> run_spmm(const CsrMatrix& a, const Dens
   detail::check(spmx_plan_info(plan.h, &parts, &chunks, nullptr));
   report.threads = parts;
   report.n_chunks = chunks;
-  if (cfg.jit_width) {  // code generation happens on the first launch for this d: keep it out of
+  if (jit) {  // code generation happens on the first launch for this d: keep it out of
     double before = 0.0, after = 0.0;  // the timed trials, like the reference's emit()
     detail::check(spmx_jit_stats(nullptr, &before));
     detail::check(spmx_spmm(c.h, plan.h, da.h, (const float*)dx.p, x.rows, d, (float*)dy.p, nullptr));

@@ -2,8 +2,8 @@
 
 Exact mode (SPMX_EXACT_ORDER): bitwise equal to the reference's run_spmm for every
 strategy and part count (checksum equality, dense.cpp:17-28).
-Default mode: rows not cut by a chunk boundary and shorter than the cooperative
-threshold are still bitwise equal; every element obeys the north_star bound
+Default mode: rows not cut by a chunk boundary (interior cuts never fall inside rows
+shorter than LONG_SEG) are still bitwise equal; every element obeys the north_star bound
 |y - y_ref| <= 1e-5 * sum|a*x| + 1e-6 against the unfused reference (reference.cpp:10-25).
 """
 import numpy as np

@@ -6,7 +6,7 @@
 //   spmx_bench_b200 [--matrix f.mtx|f.jspm | --synthetic ROWS [--avg-nnz A] [--skew S]]
 //                   [--cols D] [--strategy row|nnz|merge] [--dispatch static|dynamic]
 //                   [--backend native|interp] [--threads T] [--batch-size B] [--trials K]
-//                   [--seed S] [--verify] [--jit] [--format json|csv] [--report FILE]
+//                   [--seed S] [--verify] [--no-jit] [--format json|csv] [--report FILE]
 //                   [--save-cache f.jspm] [--peak-gbs G]
 //   spmx_bench_b200 sweep [common options] [--d-list 16 32 ...] [--strategies row nnz merge]
 //                   [--backends native interp] [--dispatch static|dynamic]
@@ -41,7 +41,7 @@ struct Cli {
   std::string strategy = "row", dispatch = "dynamic", backend = "native";
   unsigned threads = 0, trials = 1;
   uint64_t batch_size = 128, seed = 42;
-  bool verify = false, jit = false;
+  bool verify = false, jit = true;
   std::string format = "json", report_path, save_cache_path;
   double peak_gbs = 6551.0;  // measured HBM copy peak of this pool's B200s (MEASURED_PEAKS.json)
   bool sweep = false;
@@ -280,6 +280,7 @@ Cli parse(int argc, char** argv) {
     else if (key == "--seed") c.seed = std::strtoull(value().c_str(), nullptr, 10);
     else if (key == "--verify") c.verify = true;
     else if (key == "--jit") c.jit = true;
+    else if (key == "--no-jit") c.jit = false;
     else if (key == "--format") { c.format = value(); if (c.format != "json" && c.format != "csv") throw UsageError("--format: json|csv"); }
     else if (key == "--report") c.report_path = value();
     else if (key == "--peak-gbs") c.peak_gbs = std::atof(value().c_str());
