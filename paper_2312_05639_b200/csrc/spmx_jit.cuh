@@ -65,12 +65,15 @@ struct Shape {
   bool ragged;
 };
 
-// lanes per row and tiles per lane for width d: the fewest lanes that keep <= 4 tiles per lane
-// (more row groups per warp), then <= 8 tiles with all 32 lanes. d beyond that is slabbed by
-// the caller.
+// lanes per row and tiles per lane for width d: the fewest lanes (but at least 4, or the whole
+// row when it is narrower: one- and two-lane groups gather uncoalesced) that keep <= 4 tiles
+// per lane (more row groups per warp), then <= 8 tiles with all 32 lanes. d beyond that is
+// slabbed by the caller.
 inline Shape choose_shape(int d, int vec) {
   const int lanes = (d + vec - 1) / vec;
-  for (int g = 1; g <= 32; g <<= 1) {
+  int gmin = 1;
+  while (gmin < 4 && gmin < lanes) gmin <<= 1;
+  for (int g = gmin; g <= 32; g <<= 1) {
     const int nt = (lanes + g - 1) / g;
     if (nt <= (g < 32 ? 4 : 8)) return {g, vec, nt, g * nt * vec != d};
   }
