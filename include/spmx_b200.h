@@ -20,6 +20,12 @@
  * col_indices uint32, values float (include/spmx/csr.hpp:10-20). There is no
  * CPU fallback anywhere behind this ABI: without a CUDA device every compute
  * entry point fails with SPMX_ERUNTIME.
+ *
+ * Threading (executor.cpp: run_spmm holds no global state): a context and the
+ * handles created from it belong to one host thread at a time; concurrent callers use one
+ * context each (the thread_local context of INTEGRATION.md). A CSR handle may be shared by the
+ * plans of its own context only; a plan owns scratch (the carry rows) that its launches write,
+ * so two launches of the same plan must be ordered on the context's stream, which they are.
  */
 #ifndef SPMX_B200_H
 #define SPMX_B200_H
