@@ -177,16 +177,6 @@ struct SpmmArgs {
   u64 batch;
 };
 
-template <int G, int VEC, int NT, bool RAGGED>
-__device__ __forceinline__ void store_row(const SpmmArgs& a, float* dst_row, int lg,
-                                          const float (&acc)[NT][VEC], u64 pol) {
-#pragma unroll
-  for (int t = 0; t < NT; ++t) {
-    const int c = (t * G + lg) * VEC;
-    if (!RAGGED || c < a.dw) st_y<VEC>(dst_row + a.c0 + c, acc[t], pol);
-  }
-}
-
 template <int NT, int VEC>
 __device__ __forceinline__ void zero_acc(float (&acc)[NT][VEC]) {
 #pragma unroll
@@ -211,7 +201,11 @@ constexpr int kStageBatch = SPMX_STAGE_BATCH;
 // row) do better with more resident warps and a shallower pipeline.
 template <int D_CT, int NT>
 struct Tune {
+#ifdef SPMX_MIN_CTAS_RAW
+  static constexpr int kMinCtas = SPMX_MIN_CTAS_RAW;
+#else
   static constexpr int kMinCtas = ((NT <= 2) ? SPMX_MIN_CTAS : 1) * (8 / kWarpsPerCta);
+#endif
   static constexpr int kInFlight = SPMX_U;
 };
 // d = 128: four float4 tiles per lane, 8 lanes per row (4 rows per warp step instead of 2:
@@ -233,19 +227,32 @@ __host__ __device__ constexpr int pipeline_depth(int want, int g) {
   return u;
 }
 
-// Rows whose bounds one group stages at a time (shared memory: 6 bytes per row and group).
+#ifndef SPMX_REFILL_FIRST
+#define SPMX_REFILL_FIRST (-1)  // -1: per width
+#endif
+#ifndef SPMX_EARLY_FILL
+#define SPMX_EARLY_FILL 1
+#endif
+#ifndef SPMX_SHFL_AHEAD
+#define SPMX_SHFL_AHEAD 1
+#endif
+#ifndef SPMX_WINDOW_ROWS
+#define SPMX_WINDOW_ROWS 64
+#endif
+// Non-empty rows one group stages at a time (shared memory: 8 bytes per record and group).
 template <int G>
 struct Window {
   static constexpr int NGW = 32 / G;
-  static constexpr int kRows = (512 / NGW) > 128 ? 128 : (512 / NGW);
+  static constexpr int kRows = (512 / NGW) > SPMX_WINDOW_ROWS ? SPMX_WINDOW_ROWS : (512 / NGW);
 };
 
-// Per-warp shared memory: one region per group.
+// Per-warp shared memory: one region per group. One record per non-empty row of the window:
+// x = end of the row (offset from the piece's first nonzero, clipped to the piece), y = its
+// window-local row index (kCarryIdx for the row the piece ends in: its partial goes to carry_out).
+constexpr u32 kCarryIdx = 0xffffffffu;
 template <int G>
 struct WarpScratch {
-  u32 row_end[Window<G>::NGW][Window<G>::kRows];             // end of the k-th non-empty row,
-                                                             // offset from the piece's first nnz
-  unsigned short row_idx[Window<G>::NGW][Window<G>::kRows];  // its window-local row index
+  uint2 rec[Window<G>::NGW][Window<G>::kRows + 2];  // + the two records read ahead at a row end
 };
 
 // One piece of the merge path per GROUP of G lanes: the nonzeros and row ends between the
@@ -267,11 +274,21 @@ struct WarpScratch {
 // row is stored and the accumulators are zeroed. Every row that lies wholly inside a piece
 // is therefore ONE fmaf chain in CSR order: bitwise equal to the reference.
 // A piece must span fewer than 2^32 nonzeros (the plan guarantees it).
+template <int G, int VEC, int NT, bool RAGGED>
+__device__ __forceinline__ void store_lane(const SpmmArgs& a, float* dst_lane, int lg,
+                                           const float (&acc)[NT][VEC], u64 pol) {
+#pragma unroll
+  for (int t = 0; t < NT; ++t)
+    if (!RAGGED || (t * G + lg) * VEC < a.dw) st_y<VEC>(dst_lane + t * G * VEC, acc[t], pol);
+}
+
 template <int D_CT, int G, int VEC, int NT, bool RAGGED>
 __device__ __forceinline__ void process_piece(const SpmmArgs& a, bool active, u64 r0, u64 j0,
                                               u64 r1, u64 j1, float* carry_row,
                                               int lane, WarpScratch<G>& sm) {
-  constexpr int W = Window<G>::kRows;
+  constexpr int W = Window<G>::kRows;  // staged records (non-empty rows) per window
+  constexpr int kScan = 512;           // rows scanned per window
+  constexpr bool kRefillFirst = SPMX_REFILL_FIRST >= 0 ? (SPMX_REFILL_FIRST != 0) : (NT <= 2);
   // positions in flight per lane: the largest power of two with U * NT <= kInFlight, at most G
   // (so that U divides G and a position keeps its pipeline slot from batch to batch)
   constexpr int U = pipeline_depth(Tune<D_CT, NT>::kInFlight / NT, G);
@@ -281,36 +298,34 @@ __device__ __forceinline__ void process_piece(const SpmmArgs& a, bool active, u6
   const u64 row_lim = active ? r1 + (r1 < a.m ? 1 : 0) : r0;
   const u32* __restrict__ colp = a.col + j0;
   const float* __restrict__ valp = a.vals + j0;
-  const float* __restrict__ xbase = a.x + a.c0 + lg * VEC;
+  const int lane_col = a.c0 + lg * VEC;  // first column this lane owns
+  const float* __restrict__ xbase = a.x + lane_col;
+  float* const carry_lane = carry_row ? carry_row + lane_col : nullptr;
   const u32 span = active ? (u32)(j1 - j0) : 0u;
   const unsigned grp_mask = (G == 32) ? kFullMask : (((1u << G) - 1u) << (g * G));
   const unsigned lt_mask = grp_mask & ((1u << lane) - 1u);
-  u32* __restrict__ s_end = sm.row_end[g];
-  unsigned short* __restrict__ s_idx = sm.row_idx[g];
+  uint2* __restrict__ s_rec = sm.rec[g];
   float acc[NT][VEC];
   const u64 pol_first = policy_evict_first(), pol_last = policy_evict_last();
 
   u32 ws = 0;  // nonzero offset where the current window starts
-  for (u64 wbase = r0; __any_sync(kFullMask, wbase < row_lim); wbase += W) {
-    const int nw = wbase < row_lim ? (int)min((u64)W, row_lim - wbase) : 0;
-    // The window's first two column/value batches do not depend on the row bounds: fetch them
-    // now so that their latency overlaps the row_ptr loads below.
+  int adv = 0;  // rows the previous window covered
+  for (u64 wbase = r0; __any_sync(kFullMask, wbase < row_lim); wbase += adv) {
+    // A window holds at most W non-empty rows (the staged records) out of at most kScan rows:
+    // it ends where the rows of the piece end, or where the records run out.
+    const int nw = wbase < row_lim ? (int)min((u64)kScan, row_lim - wbase) : 0;
+    float* const ywin = a.y + (size_t)wbase * (size_t)ldx + lane_col;  // this lane's columns of row wbase
+    // The window's first two column/value batches and its first U gathers do not depend on the
+    // row bounds: they are issued first, so that the row_ptr loads, the staging below and the
+    // gather round trip overlap.
     const u32 p0 = ws;
     u32 c0 = 0, c1 = 0;
     float v0 = 0.0f, v1 = 0.0f;
     if (p0 + lg < span) { c0 = ld_stream(colp + p0 + lg, pol_first); v0 = ld_stream(valp + p0 + lg, pol_first); }
     if (p0 + G + lg < span) { c1 = ld_stream(colp + p0 + G + lg, pol_first); v1 = ld_stream(valp + p0 + G + lg, pol_first); }
-    // ---- stage the window: clipped row ends, compacted over non-empty rows ----------------
-    // Row ends are loaded kStageBatch * G rows at a time (all loads of a batch in flight
-    // together); a row starts where the previous one ends.
-    int count = 0;
-    u32 prev_e = ws;
-    __syncwarp();
-    zero_acc(acc);
     const int nw_max = __reduce_max_sync(kFullMask, nw);
-#pragma unroll 1
-    for (int qb = 0; qb < nw_max; qb += kStageBatch * G) {
-      u32 eb[kStageBatch];
+    u32 eb[kStageBatch];
+    auto load_bounds = [&](int qb) {
 #pragma unroll
       for (int i = 0; i < kStageBatch; ++i) {
         const int li = qb + i * G + lg;
@@ -320,54 +335,79 @@ __device__ __forceinline__ void process_piece(const SpmmArgs& a, bool active, u6
           eb[i] = hi > j0 ? (u32)min(hi - j0, (u64)span) : 0u;
         }
       }
+    };
+    load_bounds(0);
+    VecT<VEC> xv[U][NT];
+    auto fill = [&]() {
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        const u32 kq = __shfl_sync(kFullMask, c0, u, G);
+        if (p0 + (u32)u < span) {
+          const float* xr = xbase + (size_t)kq * (size_t)ldx;
+#pragma unroll
+          for (int t = 0; t < NT; ++t)
+            if (!RAGGED || (t * G + lg) * VEC < a.dw) xv[u][t] = ld_x<VEC>(xr + t * G * VEC, pol_last);
+        }
+      }
+    };
+    if (SPMX_EARLY_FILL) fill();
+    // ---- stage the window: clipped row ends, compacted over non-empty rows ----------------
+    // Row ends are loaded kStageBatch * G rows at a time (all loads of a batch in flight
+    // together); a row starts where the previous one ends.
+    int count = 0;
+    u32 prev_e = ws;
+    bool open = true;  // group-uniform: the record buffer still has room for G more rows
+    adv = nw;
+    __syncwarp();
+    zero_acc(acc);
+#pragma unroll 1
+    for (int qb = 0; qb < nw_max; qb += kStageBatch * G) {
+      if (qb > 0) {
+        if (!__any_sync(kFullMask, open && qb < nw)) break;
+        load_bounds(qb);
+      }
 #pragma unroll
       for (int i = 0; i < kStageBatch; ++i) {
         const int q0 = qb + i * G;
         if (q0 >= nw_max) break;  // warp-uniform
+        if (open && q0 < nw && count + G > W) {  // out of records: the window ends before row q0
+          open = false;
+          adv = q0;
+        }
         const int li = q0 + lg;
-        const bool valid = li < nw;
+        const bool valid = open && li < nw;
         const u32 e = eb[i];
         const u32 up = __shfl_up_sync(kFullMask, e, 1, G);
         const u32 s = lg == 0 ? prev_e : up;
         prev_e = __shfl_sync(kFullMask, e, G - 1, G);
         const unsigned ne = __ballot_sync(kFullMask, valid && e != s) & grp_mask;
-        if (valid && e != s) {
-          const int pos = count + __popc(ne & lt_mask);
-          s_idx[pos] = (unsigned short)li;
-          s_end[pos] = e;
-        }
+        if (valid && e != s)
+          s_rec[count + __popc(ne & lt_mask)] = make_uint2(e, wbase + li < r1 ? (u32)li : kCarryIdx);
         count += __popc(ne);
         // empty rows that end inside the piece: the whole group writes one row of zeros at a time
         unsigned em = __ballot_sync(kFullMask, valid && e == s && wbase + li < r1) & grp_mask;
         while (em) {
           const int src = (__ffs(em) - 1) - g * G;
           em &= em - 1;
-          store_row<G, VEC, NT, RAGGED>(a, a.y + (size_t)(wbase + q0 + src) * (size_t)ldx, lg, acc, pol_first);
+          store_lane<G, VEC, NT, RAGGED>(a, ywin + (size_t)(q0 + src) * (size_t)ldx, lg, acc, pol_first);
         }
       }
     }
     __syncwarp();
-    const u32 we = count > 0 ? s_end[count - 1] : ws;
+    const u32 we = count > 0 ? s_rec[count - 1].x : ws;
     const u32 L = we - ws;  // nonzeros of this window in this group's piece
     const u32 Lmax = __reduce_max_sync(kFullMask, L);
     if (Lmax == 0) continue;  // warp-uniform
+    if (!SPMX_EARLY_FILL) fill();
     int k = 0;  // current row = k-th non-empty row of the window
+    // the record of the current row and of the one after it are kept in registers, so that a
+    // row end costs no shared-memory round trip
+    uint2 cur = s_rec[0], nxt = s_rec[1];
     // position (relative to the current batch) of the last nonzero of the current row
     constexpr int kNoRowEnd = 0x3fffffff;
-    int e_rel = (L > 0) ? (int)min(s_end[0] - p0 - 1u, (u32)kNoRowEnd) : kNoRowEnd;
+    int e_rel = (L > 0) ? (int)min(cur.x - p0 - 1u, (u32)kNoRowEnd) : kNoRowEnd;
 
     // ---- walk the window's nonzeros ---------------------------------------------------------
-    VecT<VEC> xv[U][NT];
-#pragma unroll
-    for (int u = 0; u < U; ++u) {
-      const u32 kq = __shfl_sync(kFullMask, c0, u, G);
-      if ((u32)u < L) {
-        const float* xr = xbase + (size_t)kq * (size_t)ldx;
-#pragma unroll
-        for (int t = 0; t < NT; ++t)
-          if (!RAGGED || (t * G + lg) * VEC < a.dw) xv[u][t] = ld_x<VEC>(xr + t * G * VEC, pol_last);
-      }
-    }
 #pragma unroll 1
     for (u32 nb = 0; nb < Lmax; nb += G) {
       const int rem = (int)min(L > nb ? L - nb : 0u, 0x7fffffffu);  // positions this group has left
@@ -378,12 +418,27 @@ __device__ __forceinline__ void process_piece(const SpmmArgs& a, bool active, u6
         v2 = ld_stream(valp + p0 + nb + 2 * G + lg, pol_first);
       }
 
+      // The broadcasts of position t + 1 are issued before position t is consumed, so that the
+      // shuffle latency is off the per-position critical path.
+      float vq = 0.0f;
+      u32 kq = 0;
+      if (SPMX_SHFL_AHEAD) {
+        vq = __shfl_sync(kFullMask, v0, 0, G);
+        kq = (U < G) ? __shfl_sync(kFullMask, c0, U % G, G) : __shfl_sync(kFullMask, c1, 0, G);
+      }
 #pragma unroll
       for (int t = 0; t < G; ++t) {
         const int u = t % U;
-        const float vq = __shfl_sync(kFullMask, v0, t, G);
-        const u32 kq = (t + U < G) ? __shfl_sync(kFullMask, c0, t + U, G)
-                                   : __shfl_sync(kFullMask, c1, t + U - G, G);
+        float vq_n = 0.0f;
+        u32 kq_n = 0;
+        if (!SPMX_SHFL_AHEAD) {
+          vq = __shfl_sync(kFullMask, v0, t, G);
+          kq = (t + U < G) ? __shfl_sync(kFullMask, c0, t + U, G) : __shfl_sync(kFullMask, c1, t + U - G, G);
+        } else if (t + 1 < G) {
+          vq_n = __shfl_sync(kFullMask, v0, t + 1, G);
+          kq_n = (t + 1 + U < G) ? __shfl_sync(kFullMask, c0, t + 1 + U, G)
+                                 : __shfl_sync(kFullMask, c1, t + 1 + U - G, G);
+        }
         if (t < rem) {
 #pragma unroll
           for (int tt = 0; tt < NT; ++tt)
@@ -393,20 +448,33 @@ __device__ __forceinline__ void process_piece(const SpmmArgs& a, bool active, u6
                 acc[tt][e] = __fmaf_rn(vq, xv[u][tt].v[e], acc[tt][e]);
             }
         }
-        if (t == e_rel) {  // row k ends here: store it, start the next one
-          const u64 rr = wbase + s_idx[k];
-          float* dst = (rr < r1) ? a.y + (size_t)rr * (size_t)ldx : carry_row;
-          store_row<G, VEC, NT, RAGGED>(a, dst, lg, acc, pol_first);
-          zero_acc(acc);
-          ++k;
-          e_rel = (k < count) ? (int)min((u32)e_rel + (s_end[k] - s_end[k - 1]), (u32)kNoRowEnd) : kNoRowEnd;
-        }
-        if (t + U < rem) {
+        // the slot is free again: refill it before any row-end work (with four tiles per lane
+        // the compiler turns this order into three branches per position: refill afterwards)
+        if (kRefillFirst && t + U < rem) {
           const float* xr = xbase + (size_t)kq * (size_t)ldx;
 #pragma unroll
           for (int tt = 0; tt < NT; ++tt)
             if (!RAGGED || (tt * G + lg) * VEC < a.dw) xv[u][tt] = ld_x<VEC>(xr + tt * G * VEC, pol_last);
         }
+        if (t == e_rel) {  // row k ends here: store it, start the next one
+          float* dst = (cur.y != kCarryIdx) ? ywin + (size_t)cur.y * (size_t)ldx : carry_lane;
+          store_lane<G, VEC, NT, RAGGED>(a, dst, lg, acc, pol_first);
+          zero_acc(acc);
+          ++k;
+          e_rel = (k < count) ? (int)min((u32)e_rel + (nxt.x - cur.x), (u32)kNoRowEnd) : kNoRowEnd;
+          // (the copies are pinned inside the branch: the compiler otherwise hoists them in
+          // front of every position's row-end test)
+          asm volatile("mov.b32 %0, %2;\n\tmov.b32 %1, %3;" : "=r"(cur.x), "=r"(cur.y) : "r"(nxt.x), "r"(nxt.y));
+          nxt = s_rec[k + 1];
+        }
+        if (!kRefillFirst && t + U < rem) {
+          const float* xr = xbase + (size_t)kq * (size_t)ldx;
+#pragma unroll
+          for (int tt = 0; tt < NT; ++tt)
+            if (!RAGGED || (tt * G + lg) * VEC < a.dw) xv[u][tt] = ld_x<VEC>(xr + tt * G * VEC, pol_last);
+        }
+        vq = vq_n;
+        kq = kq_n;
       }
       c0 = c1; v0 = v1;
       c1 = c2; v1 = v2;
