@@ -177,6 +177,37 @@ struct SpmmArgs {
   u64 batch;
 };
 
+// acc[e] = fma(v, x[e], acc[e]) with one rounding per element (src/interp.cpp:43). Blackwell's
+// packed FFMA2 (fma.rn.f32x2: two independent IEEE fp32 FMAs per instruction, bitwise equal
+// to two scalar FMAs) halves the instruction count of the reduce step.
+#ifndef SPMX_FFMA2
+#define SPMX_FFMA2 1
+#endif
+__device__ __forceinline__ void fma2(float v, float x0, float x1, float& a0, float& a1) {
+#if SPMX_FFMA2
+  unsigned long long vv, xx, aa;
+  asm("mov.b64 %0, {%1, %1};" : "=l"(vv) : "f"(v));
+  asm("mov.b64 %0, {%1, %2};" : "=l"(xx) : "f"(x0), "f"(x1));
+  asm("mov.b64 %0, {%1, %2};" : "=l"(aa) : "f"(a0), "f"(a1));
+  asm("fma.rn.f32x2 %0, %1, %2, %0;" : "+l"(aa) : "l"(vv), "l"(xx));
+  asm("mov.b64 {%0, %1}, %2;" : "=f"(a0), "=f"(a1) : "l"(aa));
+#else
+  a0 = __fmaf_rn(v, x0, a0);
+  a1 = __fmaf_rn(v, x1, a1);
+#endif
+}
+template <int VEC>
+__device__ __forceinline__ void fma_tile(float v, const VecT<VEC>& x, float (&acc)[VEC]) {
+  if constexpr (VEC == 4) {
+    fma2(v, x.v[0], x.v[1], acc[0], acc[1]);
+    fma2(v, x.v[2], x.v[3], acc[2], acc[3]);
+  } else if constexpr (VEC == 2) {
+    fma2(v, x.v[0], x.v[1], acc[0], acc[1]);
+  } else {
+    acc[0] = __fmaf_rn(v, x.v[0], acc[0]);
+  }
+}
+
 template <int NT, int VEC>
 __device__ __forceinline__ void zero_acc(float (&acc)[NT][VEC]) {
 #pragma unroll
@@ -443,9 +474,7 @@ __device__ __forceinline__ void process_piece(const SpmmArgs& a, bool active, u6
 #pragma unroll
           for (int tt = 0; tt < NT; ++tt)
             if (!RAGGED || (tt * G + lg) * VEC < a.dw) {
-#pragma unroll
-              for (int e = 0; e < VEC; ++e)
-                acc[tt][e] = __fmaf_rn(vq, xv[u][tt].v[e], acc[tt][e]);
+              fma_tile<VEC>(vq, xv[u][tt], acc[tt]);
             }
         }
         // the slot is free again: refill it before any row-end work (with four tiles per lane
