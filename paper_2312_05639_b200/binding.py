@@ -70,6 +70,13 @@ def build_library(force: bool = False, verbose: bool = False) -> str:
     if verbose:
         print(" ".join(cmd), file=sys.stderr)
     subprocess.check_call(cmd)
+    # second scoreboard for half of the walk loop's gathers (sass_sched.py):
+    # applied only when its preconditions hold, SPMX_NO_SASS_SCHED=1 leaves the kernels as compiled
+    if not os.environ.get("SPMX_NO_SASS_SCHED"):
+        from . import sass_sched
+        say = (lambda m: print("sass_sched:", m, file=sys.stderr)) if verbose else (lambda m: None)
+        n = sass_sched.patch_library(LIB_PATH, log=say)
+        say(f"{n} kernel(s) re-scheduled")
     return LIB_PATH
 
 

@@ -215,6 +215,16 @@ __device__ __forceinline__ void zero_acc(float (&acc)[NT][VEC]) {
 #pragma unroll
     for (int v = 0; v < VEC; ++v) acc[t][v] = 0.0f;
 }
+// The same inside the row-end branch, from a register that holds zero: ptxas otherwise
+// materialises every constant zero there through a uniform register (two instructions per
+// accumulator).
+template <int NT, int VEC>
+__device__ __forceinline__ void zero_acc_from(float (&acc)[NT][VEC], float zero) {
+#pragma unroll
+  for (int t = 0; t < NT; ++t)
+#pragma unroll
+    for (int v = 0; v < VEC; ++v) acc[t][v] = zero;
+}
 
 #ifndef SPMX_U
 #define SPMX_U 16  // LDG.128 gathers in flight per lane (measured best with 2 CTAs/SM)
@@ -337,6 +347,7 @@ __device__ __forceinline__ void process_piece(const SpmmArgs& a, bool active, u6
   const unsigned lt_mask = grp_mask & ((1u << lane) - 1u);
   uint2* __restrict__ s_rec = sm.rec[g];
   float acc[NT][VEC];
+  const float zero_f = __int_as_float(a.dw >> 31);  // 0.0f (dw >= 0), opaque to the compiler
   const u64 pol_first = policy_evict_first(), pol_last = policy_evict_last();
 
   u32 ws = 0;  // nonzero offset where the current window starts
@@ -488,7 +499,7 @@ __device__ __forceinline__ void process_piece(const SpmmArgs& a, bool active, u6
         if (t == e_rel) {  // row k ends here: store it, start the next one
           float* dst = (cur.y != kCarryIdx) ? ywin + (size_t)cur.y * (size_t)ldx : carry_lane;
           store_lane<G, VEC, NT, RAGGED>(a, dst, lg, acc, pol_first);
-          zero_acc(acc);
+          zero_acc_from(acc, zero_f);
           ++k;
           e_rel = (k < count) ? (int)min((u32)e_rel + (nxt.x - cur.x), (u32)kNoRowEnd) : kNoRowEnd;
           // (the copies are pinned inside the branch: the compiler otherwise hoists them in
