@@ -104,6 +104,21 @@ __device__ __forceinline__ VecT<VEC> ld_x(const float* p, u64 pol) {
   return r;
 }
 
+// software prefetch of the col/val stream (a line = 32 positions)
+#ifndef SPMX_PF_STREAM
+#define SPMX_PF_STREAM 0  // 0 off, 1 prefetch.global.L2, 2 prefetch.global.L1
+#endif
+#ifndef SPMX_PF_DIST
+#define SPMX_PF_DIST 64  // positions ahead of the newest col/val batch
+#endif
+__device__ __forceinline__ void pf_stream(const void* p) {
+#if SPMX_PF_STREAM == 1
+  asm volatile("prefetch.global.L2 [%0];" ::"l"(p));
+#elif SPMX_PF_STREAM == 2
+  asm volatile("prefetch.global.L1 [%0];" ::"l"(p));
+#endif
+}
+
 // streaming loads of the CSR arrays
 __device__ __forceinline__ u32 ld_stream(const u32* p, u64 pol) {
 #if SPMX_POL_STREAM
@@ -365,6 +380,12 @@ __device__ __forceinline__ void process_piece(const SpmmArgs& a, bool active, u6
     float v0 = 0.0f, v1 = 0.0f;
     if (p0 + lg < span) { c0 = ld_stream(colp + p0 + lg, pol_first); v0 = ld_stream(valp + p0 + lg, pol_first); }
     if (p0 + G + lg < span) { c1 = ld_stream(colp + p0 + G + lg, pol_first); v1 = ld_stream(valp + p0 + G + lg, pol_first); }
+#if SPMX_PF_STREAM
+    {  // the lines that hold positions [p0 + 2G, p0 + 2G + SPMX_PF_DIST): one line per lane and array
+      const u32 q = p0 + 2 * G + 32 * (u32)lg;
+      if (32 * lg < SPMX_PF_DIST && q < span) { pf_stream(colp + q); pf_stream(valp + q); }
+    }
+#endif
     const int nw_max = __reduce_max_sync(kFullMask, nw);
     u32 eb[kStageBatch];
     auto load_bounds = [&](int qb) {
@@ -459,6 +480,13 @@ __device__ __forceinline__ void process_piece(const SpmmArgs& a, bool active, u6
         c2 = ld_stream(colp + p0 + nb + 2 * G + lg, pol_first);
         v2 = ld_stream(valp + p0 + nb + 2 * G + lg, pol_first);
       }
+#if SPMX_PF_STREAM
+      if ((nb & 31u) == 0) {  // warp-uniform: once per line
+        const u32 q = p0 + nb + 2 * G + SPMX_PF_DIST;
+        if (lg == 0 && q < span) pf_stream(colp + q);
+        if (lg == 1 && q < span) pf_stream(valp + q);
+      }
+#endif
 
       // The broadcasts of position t + 1 are issued before position t is consumed, so that the
       // shuffle latency is off the per-position critical path.

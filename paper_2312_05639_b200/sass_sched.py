@@ -122,6 +122,41 @@ def _read_regs(ins):
     return regs
 
 
+def _free_store_barrier(body, sb, target):
+    """Edits {index: hi word} that move every use of scoreboard `sb` inside the loop body to
+    `target`, or None unless all of them are (STG read barrier, first later waiter in the same
+    straight-line run) pairs."""
+    if any(c.wb == sb for c in body):
+        return None
+    edits = {}
+    paired = set()
+    for k, c in enumerate(body):
+        if c.rb != sb:
+            continue
+        if not re.search(r"\bSTG\b|\bSTG\.", c.text):
+            return None
+        j = k + 1
+        while j < len(body) and j <= k + 24:
+            t = body[j].text
+            if re.search(r"\b(BRA|BSYNC|BSSY|EXIT|CALL|RET)\b", t):
+                return None
+            if body[j].rb == sb:
+                return None
+            if body[j].wait >> sb & 1:
+                break
+            j += 1
+        else:
+            return None
+        edits[k] = (c.hi & ~(7 << 49)) | (target << 49)
+        edits[j] = (body[j].hi & ~(1 << (52 + sb))) | (1 << (52 + target))
+        paired.add(j)
+    if not edits:
+        return None
+    if any((c.wait >> sb & 1) and k not in paired for k, c in enumerate(body)):
+        return None
+    return edits
+
+
 def plan_patch(code, log=None):
     """Returns a list of (instruction index, new hi word) or None when a precondition fails."""
     say = log or (lambda s: None)
@@ -159,6 +194,17 @@ def plan_patch(code, log=None):
             used.add(c.rb)
         used |= {b for b in range(6) if c.wait >> b & 1}
     free = [sb for sb in (4, 3) if sb not in used]
+    pre_edits = {}
+    if not free:
+        # A scoreboard whose only use inside the loop is "STG holds its source registers /
+        # the next writer of those registers waits" (the row-end store) can share the
+        # scoreboard of another short-lived producer: both sides of every pair are moved.
+        for sb in (4, 3):
+            pre_edits = _free_store_barrier(body, sb, target=1)
+            if pre_edits is not None:
+                free = [sb]
+                say(f"SB{sb} freed: {len(pre_edits) // 2} row-end store barriers moved to SB1")
+                break
     if not free:
         say(f"no free scoreboard in the loop (used {sorted(used)})")
         return None
@@ -191,8 +237,11 @@ def plan_patch(code, log=None):
         if _read_regs(c) & moved:
             say("early reader of a moved destination")
             return None
-    edits = [(top + k, body[k].with_wb(sb)) for k in half]
-    edits.append((top + wait_at, body[wait_at].with_wait(sb)))
+    his = {k: hi for k, hi in (pre_edits or {}).items()}
+    for k in half:
+        his[k] = (his.get(k, body[k].hi) & ~(7 << 46)) | (sb << 46)
+    his[wait_at] = his.get(wait_at, body[wait_at].hi) | (1 << (52 + sb))
+    edits = [(top + k, hi) for k, hi in sorted(his.items())]
     say(f"loop {code[top].addr:#x}..{code[end].addr:#x}: {len(half)} of {len(loads)} gathers -> SB{sb}, "
         f"wait added at {body[wait_at].addr:#x} ({body[wait_at].text.split()[1] if body[wait_at].text.startswith('@') else body[wait_at].text.split()[0]})")
     return edits
