@@ -209,46 +209,68 @@ def plan_patch(code, log=None):
         say(f"no free scoreboard in the loop (used {sorted(used)})")
         return None
     sb = free[0]
-    # consumers: first reader (in program order from the loop top) of each gather's destination
-    first_read = {}
+    # consumer of a gather: the first instruction after it, cyclically through the loop body,
+    # that reads one of its destination registers
+    n = len(body)
+    cons = {}
     for k in loads:
         d = _dest_regs(body[k])
         if not d:
             say("cannot parse a gather's destination")
             return None
-        r = next((j for j, c in enumerate(body) if j != k and "LDG" not in c.text and _read_regs(c) & d), None)
-        if r is None or r > k:
-            say("a gather's consumer does not precede its re-issue inside the loop")
+        r = next((j % n for j in range(k + 1, k + n) if "LDG" not in body[j % n].text and _read_regs(body[j % n]) & d),
+                 None)
+        if r is None:
+            say("a gather without a consumer inside the loop")
             return None
-        first_read[k] = r
-    order = sorted(loads, key=lambda k: (first_read[k], k))
-    half = order[len(order) // 2:]  # refills of the second half of the slots
-    wait_at = min(first_read[k] for k in half)
-    # every first-half consumer must come before the new wait, every moved load after it
-    if any(first_read[k] >= wait_at for k in order[:len(order) // 2]):
-        say("consumers of the two halves interleave")
+        cons[k] = r
+    # refill events in issue order (one per gather instruction: the gathers of one position
+    # are consecutive events with consecutive consumers, so halves of the pipeline depth fall on
+    # position boundaries)
+    events = []
+    for k in loads:
+        if events and cons[events[-1][0]] == cons[k]:
+            events[-1].append(k)
+        else:
+            events.append([k])
+    m = len(events)
+    # pipeline depth in events: how many refill events are issued between an event and its consumer
+    def dist(k, j):
+        return (j - k) % n
+    depth = sum(1 for e in events if 0 < dist(events[0][0], e[0]) < dist(events[0][0], cons[events[0][0]])) + 1
+    if depth < 2 or m % depth or depth % 2:
+        say(f"unexpected pipeline shape ({m} refill events, depth {depth})")
         return None
-    if any(k < wait_at for k in half):
-        say("a moved gather is issued before the new wait")
-        return None
-    # no instruction between the loop top and the wait may touch the moved destinations
-    moved = set().union(*[_dest_regs(body[k]) for k in half])
-    for c in body[:wait_at]:
-        if _read_regs(c) & moved:
-            say("early reader of a moved destination")
-            return None
+    halfd = depth // 2
+    moved_events = [t for t in range(m) if (t // halfd) % 2 == 1]
     his = {k: hi for k, hi in (pre_edits or {}).items()}
-    for k in half:
-        his[k] = (his.get(k, body[k].hi) & ~(7 << 46)) | (sb << 46)
-    his[wait_at] = his.get(wait_at, body[wait_at].hi) | (1 << (52 + sb))
+    waits = []
+    for t in moved_events:
+        for k in events[t]:
+            his[k] = (his.get(k, body[k].hi) & ~(7 << 46)) | (sb << 46)
+        if (t - 1) not in moved_events:  # first event of a run: its consumer waits for the run
+            waits.append(cons[events[t][0]])
+    for w in waits:
+        his[w] = his.get(w, body[w].hi) | (1 << (52 + sb))
+    # every moved gather needs one of the new waits after its issue and not after its consumer,
+    # and no gather on the new scoreboard may be issued between a run's last gather and its wait
+    # ... by a later run (that would drain freshly issued loads): runs alternate with SB5 runs
+    for t in moved_events:
+        for k in events[t]:
+            if not any(0 < dist(k, w) <= dist(k, cons[k]) for w in waits):
+                say("a moved gather would not be waited for")
+                return None
     edits = [(top + k, hi) for k, hi in sorted(his.items())]
-    say(f"loop {code[top].addr:#x}..{code[end].addr:#x}: {len(half)} of {len(loads)} gathers -> SB{sb}, "
-        f"wait added at {body[wait_at].addr:#x} ({body[wait_at].text.split()[1] if body[wait_at].text.startswith('@') else body[wait_at].text.split()[0]})")
+    half = [k for t in moved_events for k in events[t]]
+    wait_at = waits[0]
+    say(f"loop {code[top].addr:#x}..{code[end].addr:#x}: {len(half)} of {len(loads)} gathers -> SB{sb} "
+        f"(pipeline depth {depth} gathers), waits added at {', '.join(hex(body[w].addr) for w in waits)}")
     return edits
 
 
 def patch_library(lib, kernels=("spmm_chunk_kernelILi64ELi8ELi4ELi2ELb0", "spmm_dynamic_kernelILi64ELi8ELi4ELi2ELb0",
-                                "spmm_chunk_kernelILi32ELi8ELi4ELi1ELb0", "spmm_dynamic_kernelILi32ELi8ELi4ELi1ELb0"),
+                                "spmm_chunk_kernelILi32ELi8ELi4ELi1ELb0", "spmm_dynamic_kernelILi32ELi8ELi4ELi1ELb0",
+                                "spmm_chunk_kernelILi128ELi8ELi4ELi4ELb0", "spmm_dynamic_kernelILi128ELi8ELi4ELi4ELb0"),
                   dry_run=False, log=print):
     funcs = disassemble(lib)
     data = bytearray(open(lib, "rb").read())
