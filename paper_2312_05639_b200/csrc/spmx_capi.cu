@@ -128,6 +128,9 @@ struct spmx_plan {
   uint32_t* long_buf = nullptr;     // [count | boundaries closing chains longer than kLongChain]
   uint32_t* long_list = nullptr;    // = long_buf + 1
   uint32_t n_long = 0;
+  uint32_t* short_buf = nullptr;    // [count | boundaries closing the other chains]
+  uint32_t* short_list = nullptr;   // = short_buf + 1
+  uint32_t n_short = 0;
   u64* counter = nullptr;    // dynamic dispatch
   bool may_carry = false;
   mutable float* carry = nullptr;  // n_chunks x ld floats, grown on demand
@@ -324,7 +327,8 @@ void launch_fixup(const spmx_plan* p, u64 tb, u64 te, float* d_y, int ldx, int c
   int lpc = 1;  // lanes per chain: enough to cover the slab once, at most a warp
   while (lpc < 32 && lpc * vec < dw) lpc *= 2;
   constexpr int kT = spmx_dev::kFixupThreads;
-  const unsigned grid = p->n_long + blocks_for((te - tb) * (u64)lpc, kT);
+  if (p->n_long + p->n_short == 0) return;  // no row is cut: nothing to add
+  const unsigned grid = p->n_long + blocks_for((u64)p->n_short * (u64)lpc, kT);
   // Programmatic stream serialisation: the grid may start while the SpMM kernel before it on
   // the stream is draining; it waits (griddepcontrol.wait) before it reads that kernel's output.
   cudaLaunchConfig_t cfg{};
@@ -339,15 +343,19 @@ void launch_fixup(const spmx_plan* p, u64 tb, u64 te, float* d_y, int ldx, int c
   const uint32_t* cf = p->chain_first;
   const u64* cr = p->chunk_row;
   const uint32_t* ll = p->long_list;
+  const uint32_t* sl = p->short_list;
   const float* carry = p->carry;
   if (vec == 4)
-    CUDA_CHECK(cudaLaunchKernelEx(&cfg, spmx_dev::carry_fixup_kernel<4>, cf, cr, ll, p->n_long, tb, te,
+    CUDA_CHECK(cudaLaunchKernelEx(&cfg, spmx_dev::carry_fixup_kernel<4>, cf, cr, ll, p->n_long, sl,
+                                  p->n_short, tb, te,
                                   carry, d_y, ldx, c0, dw, lpc));
   else if (vec == 2)
-    CUDA_CHECK(cudaLaunchKernelEx(&cfg, spmx_dev::carry_fixup_kernel<2>, cf, cr, ll, p->n_long, tb, te,
+    CUDA_CHECK(cudaLaunchKernelEx(&cfg, spmx_dev::carry_fixup_kernel<2>, cf, cr, ll, p->n_long, sl,
+                                  p->n_short, tb, te,
                                   carry, d_y, ldx, c0, dw, lpc));
   else
-    CUDA_CHECK(cudaLaunchKernelEx(&cfg, spmx_dev::carry_fixup_kernel<1>, cf, cr, ll, p->n_long, tb, te,
+    CUDA_CHECK(cudaLaunchKernelEx(&cfg, spmx_dev::carry_fixup_kernel<1>, cf, cr, ll, p->n_long, sl,
+                                  p->n_short, tb, te,
                                   carry, d_y, ldx, c0, dw, lpc));
   post_launch();
 }
@@ -444,6 +452,7 @@ void plan_free(spmx_plan* p) {
   dev_free_async(p->ctx, p->work);
   dev_free_async(p->ctx, p->chain_first);
   dev_free_async(p->ctx, p->long_buf);
+  dev_free_async(p->ctx, p->short_buf);
   dev_free_async(p->ctx, p->chunk_nnz);
   dev_free_async(p->ctx, p->counter);
   dev_free_async(p->ctx, p->carry);
@@ -536,16 +545,23 @@ spmx_plan* plan_build(spmx_ctx* ctx, const spmx_csr* a, int strategy, unsigned p
       p->long_buf = dev_alloc_async<uint32_t>(ctx, long_cap + 1);
       p->long_list = p->long_buf + 1;
       CUDA_CHECK(cudaMemsetAsync(p->long_buf, 0, sizeof(uint32_t), ctx->stream));
+      p->short_buf = dev_alloc_async<uint32_t>(ctx, (size_t)total + 1);
+      p->short_list = p->short_buf + 1;
+      CUDA_CHECK(cudaMemsetAsync(p->short_buf, 0, sizeof(uint32_t), ctx->stream));
       spmx_dev::chain_first_kernel<<<blocks_for(total), 256, 0, ctx->stream>>>(
           a->row_ptr, p->chunk_row, p->chunk_nnz, total, m, p->chain_first, p->long_list,
-          p->long_buf);
+          p->long_buf, p->short_list, p->short_buf);
       post_launch();
       CUDA_CHECK(cudaMemcpyAsync(&p->n_long, p->long_buf, sizeof(uint32_t), cudaMemcpyDeviceToHost,
+                                 ctx->stream));
+      CUDA_CHECK(cudaMemcpyAsync(&p->n_short, p->short_buf, sizeof(uint32_t), cudaMemcpyDeviceToHost,
                                  ctx->stream));
       CUDA_CHECK(cudaStreamSynchronize(ctx->stream));
       dev_free_async(ctx, d_cnt);
       dev_free_async(ctx, d_off);
-      p->may_carry = true;
+      // a piece ends inside a row only where a chain of carries exists: without chains no
+      // carry is ever written and the fix-up has nothing to do
+      p->may_carry = p->n_long + p->n_short > 0;
     }
     if (p->n_chunks > 0) {
       p->work = dev_alloc_async<spmx_dev::WorkItem>(ctx, (size_t)p->n_chunks);

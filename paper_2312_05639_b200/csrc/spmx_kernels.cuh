@@ -641,14 +641,17 @@ constexpr u32 kNoChain = 0xffffffffu;
 
 // first[t], t in [0, n_chunks - 1): boundary t+1 (between chunks t and t+1) lies inside row
 // r = chunk_row[t+1] and chunk t+1 ends that row -> the chunk holding the row's first nonzero.
-// Boundaries that close a chain of more than kLongChain partials are also appended to
-// long_list (in no particular order; the chains are independent of each other).
+// Boundaries that close a chain are also appended to a list — long_list for chains of more
+// than kLongChain partials, short_list for the others (in no particular order; the chains
+// are independent of each other) — so that the fix-up grid is sized by the number of chains,
+// not by the number of boundaries.
 constexpr u32 kLongChain = 16;
 
 __global__ void chain_first_kernel(const u64* __restrict__ row_ptr, const u64* __restrict__ chunk_row,
                                    const u64* __restrict__ chunk_nnz, u64 n_chunks, u64 m,
                                    u32* __restrict__ first, u32* __restrict__ long_list,
-                                   u32* __restrict__ long_count) {
+                                   u32* __restrict__ long_count, u32* __restrict__ short_list,
+                                   u32* __restrict__ short_count) {
   const u64 t = (u64)blockIdx.x * blockDim.x + threadIdx.x;
   if (t >= n_chunks) return;
   u32 out = kNoChain;
@@ -664,6 +667,7 @@ __global__ void chain_first_kernel(const u64* __restrict__ row_ptr, const u64* _
         }
         out = (u32)lo;
         if (t - lo + 1 > kLongChain) long_list[atomicAdd(long_count, 1u)] = (u32)t;
+        else short_list[atomicAdd(short_count, 1u)] = (u32)t;
       }
     }
   }
@@ -700,15 +704,17 @@ __device__ __forceinline__ VecT<VEC> chain_sum(const float* __restrict__ src_c, 
 // The first n_long CTAs take one long chain each (more than kLongChain partials): the chain is
 // cut into blockDim/lpc consecutive segments, one per group of lpc lanes, each summed in CSR
 // order; the segment sums are then added in order. The other CTAs give one group of `lpc`
-// lanes (a power of two, <= 32) to every chunk boundary: lane lg sums columns lg*VEC .. of
-// the short chain closed by that boundary, if any, in CSR order. Both orders are fixed by the
-// plan, so the result is deterministic.
+// lanes (a power of two, <= 32) to every entry of short_list: lane lg sums columns lg*VEC ..
+// of the short chain closed by that boundary, in CSR order. Both orders are fixed by the
+// plan, so the result is deterministic. Only chains closed by a boundary t+1 with t in
+// [t_begin, t_end) are handled (the host pipeline runs the fix-up block by block).
 constexpr int kFixupThreads = 256;
 
 template <int VEC>
 __global__ void __launch_bounds__(kFixupThreads)
 carry_fixup_kernel(const u32* __restrict__ chain_first, const u64* __restrict__ chunk_row,
-                   const u32* __restrict__ long_list, u32 n_long, u64 t_begin, u64 t_end,
+                   const u32* __restrict__ long_list, u32 n_long,
+                   const u32* __restrict__ short_list, u32 n_short, u64 t_begin, u64 t_end,
                    const float* __restrict__ carry_out, float* __restrict__ y, int ldx, int c0,
                    int dw, int lpc) {
   if (blockIdx.x < n_long) {
@@ -742,12 +748,13 @@ carry_fixup_kernel(const u32* __restrict__ chain_first, const u64* __restrict__ 
     return;
   }
   const u64 tid = (u64)(blockIdx.x - n_long) * kFixupThreads + threadIdx.x;
-  // chunk whose END boundary this group inspects; boundaries t+1 for t in [t_begin, t_end)
-  const u64 last = t_begin + tid / (unsigned)lpc;
+  const u64 entry = tid / (unsigned)lpc;
   const int lg = (int)(tid % (unsigned)lpc);
-  if (last >= t_end) return;
+  if (entry >= n_short) return;
+  // chunk whose END boundary closes this chain
+  const u64 last = __ldg(short_list + entry);
+  if (last < t_begin || last >= t_end) return;
   const u32 u0 = __ldg(chain_first + last);
-  if (u0 == kNoChain || last - u0 + 1 > kLongChain) return;
   const u64 rr = __ldg(chunk_row + last + 1);
   asm volatile("griddepcontrol.wait;" ::: "memory");  // plan data above, SpMM results below
   for (int c = lg * VEC; c < dw; c += lpc * VEC) {
