@@ -523,8 +523,16 @@ spmx_plan* plan_build(spmx_ctx* ctx, const spmx_csr* a, int strategy, unsigned p
     } else {
       u64* d_cnt = dev_alloc_async<u64>(ctx, parts);
       u64* d_off = dev_alloc_async<u64>(ctx, (size_t)parts + 1);
+      // Tail taper: the last wave of the grid is cut into half-size chunks and its last third
+      // into quarter-size chunks, so that the SMs run dry together (one wave = the chunks
+      // resident at once, 64 per SM).
+      const u64 ci = chunk_items_for(m + nnz, ctx->sm_count);
+      const u64 wave = (u64)ctx->sm_count * 64 * ci;
+      const u64 taper2 = wave * env_u64("SPMX_TAPER2_WAVES", 80) / 100;
+      const u64 taper4 = wave * env_u64("SPMX_TAPER4_WAVES", 25) / 100;
       spmx_dev::count_chunks_kernel<<<blocks_for(parts), 256, 0, ctx->stream>>>(
-          d_diag, parts, chunk_items_for(m + nnz, ctx->sm_count), d_cnt);
+          d_diag, parts, ci, (m + nnz) - std::min<u64>(taper2, (m + nnz) / 4),
+          (m + nnz) - std::min<u64>(taper4, (m + nnz) / 12), d_cnt);
       post_launch();
       spmx_dev::exclusive_scan_kernel<<<1, 1024, 0, ctx->stream>>>(d_cnt, parts, d_off);
       post_launch();

@@ -113,10 +113,14 @@ __global__ void boundaries_to_diagonals_kernel(const u64* __restrict__ row_ptr,
 // Work-list refinement: a strategy range of `items` merge items becomes
 // max(1, ceil(items / chunk_items)) chunks.
 __global__ void count_chunks_kernel(const u64* __restrict__ diag, u64 parts, u64 chunk_items,
-                                    u64* __restrict__ cnt) {
+                                    u64 taper2, u64 taper4, u64* __restrict__ cnt) {
   const u64 t = (u64)blockIdx.x * blockDim.x + threadIdx.x;
   if (t >= parts) return;
   const u64 items = diag[t + 1] - diag[t];
+  // the ranges launched last are cut finer (half- and quarter-size chunks from diagonals
+  // taper2 and taper4 on): the grid's tail then ends on short pieces
+  if (diag[t] >= taper4) chunk_items = max(chunk_items / 4, (u64)32);
+  else if (diag[t] >= taper2) chunk_items = max(chunk_items / 2, (u64)32);
   const u64 c = (items + chunk_items - 1) / chunk_items;
   cnt[t] = c ? c : 1;
 }
