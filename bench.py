@@ -38,6 +38,11 @@ METRIC = "spmm_gflops"
 UNIT = "GFLOP/s"
 
 
+# L2 -> SM ceiling of this pool's B200 (whole chip, any access shape, buffer resident in L2):
+# 19.4-20.4 TB/s = 68-71 bytes per clock and SM (tools/microbench/l2_fill.cu)
+L2_TO_SM_PEAK_TBS = 20.4
+
+
 def load_peaks():
     p = os.path.join(ROOT, "MEASURED_PEAKS.json")
     try:
@@ -311,6 +316,15 @@ def main():
                 "frac": achieved / (peak * world), "traffic": traffic,
                 "algorithmic_bytes": bytes_alg, "peak_source": peak_src,
                 "kernel": "spmm_chunk_kernel (+ carry_fixup_kernel), one launch pair per step"}
+    # Second view: the kernel gathers one X row (4*d bytes) per nonzero through the L2 -> SM
+    # path, whose ceiling on this GPU is measured by tools/microbench/l2_fill.cu
+    # (profiles/r01_microbench_l2_fill.txt): what bounds the kernel in practice.
+    gather_bytes = 4.0 * nnz_total * d
+    roofline["gather"] = {"bytes": gather_bytes, "achieved_tbs": gather_bytes / (ms_step * 1e-3) / 1e12,
+                          "l2_to_sm_peak_tbs": L2_TO_SM_PEAK_TBS * world,
+                          "frac": gather_bytes / (ms_step * 1e-3) / 1e12 / (L2_TO_SM_PEAK_TBS * world),
+                          "peak_source": "measured, tools/microbench/l2_fill.cu (L2-resident buffer, "
+                                         "LDG.128, 40 warps/SM, SM clock 1.92 GHz)"}
     if world > 1:
         bytes_repl = bytes_alg + (world - 1) * 4 * n_cols * d  # X is replicated on every rank
         roofline["frac_replicated_x"] = (bytes_repl / (ms_step * 1e-3) / 1e9) / (peak * world)
