@@ -309,9 +309,18 @@ struct Window {
 // x = end of the row (offset from the piece's first nonzero, clipped to the piece), y = its
 // window-local row index (kCarryIdx for the row the piece ends in: its partial goes to carry_out).
 constexpr u32 kCarryIdx = 0xffffffffu;
+// Column indices and values reach the lanes of a group through shared memory where a group is
+// 8 lanes (the precompiled widths): every lane publishes the pair (column of position t + U,
+// value of position t) of its position once per batch, and each position is one LDS.64 —
+// half the instructions and L1 data-pipe wavefronts of two shuffles per position (shuffles
+// go through the same pipe as the gathers: at d = 32 they were a third of its load).
+#ifndef SPMX_SMEM_BCAST
+#define SPMX_SMEM_BCAST 1
+#endif
 template <int G>
 struct WarpScratch {
   uint2 rec[Window<G>::NGW][Window<G>::kRows + 2];  // + the two records read ahead at a row end
+  uint2 bc[2][G][Window<G>::NGW];  // [batch parity][position][group]: conflict-free both ways
 };
 
 // One piece of the merge path per GROUP of G lanes: the nonzeros and row ends between the
@@ -477,6 +486,8 @@ __device__ __forceinline__ void process_piece(const SpmmArgs& a, bool active, u6
     int e_rel = (L > 0) ? (int)min(cur.x - p0 - 1u, (u32)kNoRowEnd) : kNoRowEnd;
 
     // ---- walk the window's nonzeros ---------------------------------------------------------
+    constexpr bool kSmemBc = SPMX_SMEM_BCAST && G == 8 && U == G && SPMX_SHFL_AHEAD;
+    int par = 0;
 #pragma unroll 1
     for (u32 nb = 0; nb < Lmax; nb += G) {
       const int rem = (int)min(L > nb ? L - nb : 0u, 0x7fffffffu);  // positions this group has left
@@ -498,7 +509,15 @@ __device__ __forceinline__ void process_piece(const SpmmArgs& a, bool active, u6
       // shuffle latency is off the per-position critical path.
       float vq = 0.0f;
       u32 kq = 0;
-      if (SPMX_SHFL_AHEAD) {
+      uint2 (*slot)[Window<G>::NGW] = sm.bc[par];
+      if constexpr (kSmemBc) {
+        par ^= 1;
+        slot[lg][g] = make_uint2(c1, __float_as_uint(v0));  // U == G: position t + U is in the next batch
+        __syncwarp();
+        const uint2 pr = slot[0][g];
+        kq = pr.x;
+        vq = __uint_as_float(pr.y);
+      } else if (SPMX_SHFL_AHEAD) {
         vq = __shfl_sync(kFullMask, v0, 0, G);
         kq = (U < G) ? __shfl_sync(kFullMask, c0, U % G, G) : __shfl_sync(kFullMask, c1, 0, G);
       }
@@ -510,6 +529,12 @@ __device__ __forceinline__ void process_piece(const SpmmArgs& a, bool active, u6
         if (!SPMX_SHFL_AHEAD) {
           vq = __shfl_sync(kFullMask, v0, t, G);
           kq = (t + U < G) ? __shfl_sync(kFullMask, c0, t + U, G) : __shfl_sync(kFullMask, c1, t + U - G, G);
+        } else if (kSmemBc) {
+          if (t + 1 < G) {
+            const uint2 pr = slot[t + 1][g];
+            kq_n = pr.x;
+            vq_n = __uint_as_float(pr.y);
+          }
         } else if (t + 1 < G) {
           vq_n = __shfl_sync(kFullMask, v0, t + 1, G);
           kq_n = (t + 1 + U < G) ? __shfl_sync(kFullMask, c0, t + 1 + U, G)
