@@ -324,3 +324,34 @@ def test_runtime_instantiation_per_width(ctx, oracle, d):
     after = Lib.get().jit_stats()
     assert after[0] >= before[0] and after[0] >= 1   # compiled once per (device, d), then cached
     assert after[0] - before[0] <= 1
+
+
+def test_no_fixup_without_cut_rows_and_tail_taper(ctx):
+    """A plan in which no row is cut (regular matrix, rows shorter than LONG_SEG, row-granular
+    strategy boundaries) runs as ONE kernel launch per SpMM: no carry buffer, no fix-up. The
+    chunks at the end of the work list are smaller than those in its body (tail taper: the SMs
+    run dry together), and the list still covers the merge path exactly."""
+    from paper_2312_05639_b200 import workloads as W
+    from paper_2312_05639_b200.binding import Lib
+    a, x, spec = W.make_config("c3", device="cuda", m_override=1 << 17)
+    rp = a.numpy()[0]
+    da = ctx.csr_wrap(a)
+    y = torch.empty(a.m, spec["d"], device="cuda")
+    for s, max_launches in (("row", 1), ("nnz", 1), ("merge", 2)):
+        p = ctx.plan(da, s, 0)
+        ctx.spmm(p, da, x, y)
+        ctx.synchronize()
+        before = Lib.get().launch_count()
+        ctx.spmm(p, da, x, y)
+        ctx.synchronize()
+        assert 1 <= Lib.get().launch_count() - before <= max_launches, s
+        cr, cj = (v.astype(np.int64) for v in p.chunks())
+        assert cr[0] == 0 and cj[0] == 0 and cr[-1] == a.m and cj[-1] == a.nnz
+        items = np.diff(cr) + np.diff(cj)
+        assert items.min() >= 1 and items.max() <= 256 + LONG_SEG
+        body, tail = items[: len(items) // 2], items[-len(items) // 50:]
+        assert np.median(tail) <= 0.3 * np.median(body), (s, np.median(tail), np.median(body))
+        if s != "merge":
+            assert not split_row_mask(a.m, cr, cj, rp).any()
+        p.close()
+    da.close()
