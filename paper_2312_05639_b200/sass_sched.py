@@ -29,6 +29,8 @@ import sys
 
 _INSTR = re.compile(r"\s+/\*([0-9a-f]{4,})\*/\s+(.*?);\s+/\* (0x[0-9a-f]{16}) \*/")
 _HI = re.compile(r"\s+/\* (0x[0-9a-f]{16}) \*/")
+# branch with its target (plain, predicated, or uniform: "BRA.U !UP0, 0x23b0")
+_BRA = r"\bBRA(?:\.U)?\s+(?:!?UP\d+,\s*)?(0x[0-9a-f]+)"
 
 
 class Ins:
@@ -163,7 +165,7 @@ def plan_patch(code, log=None):
     # the walk loop: the backward branch whose body holds the most 128-bit constant-path gathers
     best = None
     for i, ins in enumerate(code):
-        m = re.search(r"\bBRA (0x[0-9a-f]+)", ins.text)
+        m = re.search(_BRA, ins.text)
         if not m:
             continue
         tgt = int(m.group(1), 16)
@@ -173,8 +175,8 @@ def plan_patch(code, log=None):
         if top is None:
             continue
         n = sum(1 for c in code[top:i] if "LDG.E.128.CONSTANT" in c.text)
-        inner = any(re.search(r"\bBRA (0x[0-9a-f]+)", c.text) and
-                    int(re.search(r"\bBRA (0x[0-9a-f]+)", c.text).group(1), 16) < c.addr for c in code[top:i])
+        inner = any(re.search(_BRA, c.text) and
+                    int(re.search(_BRA, c.text).group(1), 16) < c.addr for c in code[top:i])
         if n >= 4 and not inner and (best is None or n > best[2]):
             best = (top, i, n)
     if best is None:
