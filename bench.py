@@ -184,6 +184,9 @@ def main():
     ap.add_argument("--exact", action="store_true", help="SPMX_EXACT_ORDER (bitwise) mode")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--allgather", action="store_true", help="also time the all-gather of Y (N>1)")
+    ap.add_argument("--shard-by", default="nnz", choices=["nnz", "merge"],
+                    help="N>1: rank-level row blocks from split_nnz(A, G) (north_star, default) or "
+                         "split_merge(A, G) (rows + nonzeros balanced: see tools/shard_scaling.py)")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3) if args.impl == "ours" else args.warmup
 
@@ -232,7 +235,7 @@ def main():
     if world > 1:
         # nnz-balanced row shards: split_nnz(A, G) on the device, bit-exact with the reference
         da_full = ctx.csr_wrap(a_full, validate=False)
-        ranges = ctx.split_nnz(da_full, world)
+        ranges = (ctx.split_merge if args.shard_by == "merge" else ctx.split_nnz)(da_full, world)
         da_full.close()
         a, (rb, re) = sharding.local_shard(a_full, ranges, rank)
         del a_full
@@ -242,7 +245,8 @@ def main():
         e0, e1 = torch.cuda.Event(True), torch.cuda.Event(True)
         e0.record(); sharding.broadcast_x(x, 0); e1.record(); torch.cuda.synchronize()
         bcast_ms = sharding.max_over_ranks(e0.elapsed_time(e1), dev)
-        extra.update({"parallelism": f"row-shard{world}", "shard_rows": [rb, re], "x_broadcast_ms": bcast_ms})
+        extra.update({"parallelism": f"row-shard{world}", "shard_by": args.shard_by, "shard_rows": [rb, re],
+                      "x_broadcast_ms": bcast_ms})
         if share_gpu:
             extra["debug"] = "SPMX_BENCH_SHARE_GPU: all ranks on one GPU over gloo (code-path check only)"
         nnz_total = int(sharding.sum_over_ranks(a.nnz, dev))

@@ -180,6 +180,19 @@ class Context:
         self.h = h
         self.device = device
 
+    @classmethod
+    def on_torch_stream(cls, device: int = 0) -> "Context":
+        """A context whose kernels run on torch's CURRENT stream, made explicit first: the
+        legacy default stream has handle 0, which the C ABI reads as "create a private
+        (non-blocking) stream" — torch work issued before a library call (fills, slices,
+        generators) would then not be ordered with it."""
+        import torch
+        stream = torch.cuda.Stream(device=device)
+        torch.cuda.set_stream(stream)
+        c = cls(device, stream.cuda_stream)
+        c._torch_stream = stream
+        return c
+
     def close(self):
         if self.h:
             self.L.check(self.L.lib.spmx_ctx_destroy(self.h))

@@ -48,6 +48,8 @@ def ctx():
     import torch
     assert torch.cuda.is_available(), "gpu tests need a CUDA device"
     from paper_2312_05639_b200.binding import Context
-    c = Context(0)
+    # library kernels and the tests' torch work (fills, slices, generators) share one
+    # explicit stream, so they are ordered without host synchronisation
+    c = Context.on_torch_stream(0)
     yield c
     c.close()

@@ -355,3 +355,39 @@ def test_no_fixup_without_cut_rows_and_tail_taper(ctx):
             assert not split_row_mask(a.m, cr, cj, rp).any()
         p.close()
     da.close()
+
+
+def test_row_shards_on_one_device_concatenate_to_the_whole(ctx, oracle):
+    """The multi-GPU layout run on one device: A cut into the G ranges of
+    split_nnz(A, G) with rebased row_ptr, X shared, each shard multiplied on its own; the
+    concatenated Y equals the unsharded result bit for bit in exact mode (rows are never cut
+    there) and within the north_star bound in default mode."""
+    from paper_2312_05639_b200 import workloads as W
+    a, x, spec = W.make_config("c5", device="cuda", scale_override=13)
+    rp, col, vals = a.numpy()
+    xn = x.cpu().numpy()
+    want = oracle.spmm_fused(a.m, a.n, rp, col, vals, xn)
+    unf = oracle.spmm_unfused(a.m, a.n, rp, col, vals, xn)
+    bound = oracle.abs_bound(a.m, rp, col, vals, xn)
+    da = ctx.csr_wrap(a)
+    for G in (2, 4, 8):
+        ranges = ctx.split_nnz(da, G)
+        assert np.array_equal(ranges, oracle.split_nnz(rp, G))
+        assert int(ranges[0, 0]) == 0 and int(ranges[-1, 1]) == a.m
+        for flags in (EXACT, 0):
+            parts = []
+            for b, e in ranges:
+                sh = a.row_slice(int(b), int(e))
+                ds = ctx.csr_wrap(sh)
+                y = torch.full((sh.m, spec["d"]), float("nan"), device="cuda")
+                p = ctx.plan(ds, "nnz", 0, flags=flags)
+                ctx.spmm(p, ds, x, y)
+                ctx.synchronize()
+                parts.append(y.cpu().numpy())
+                p.close(); ds.close()
+            got = np.concatenate(parts, axis=0)
+            if flags == EXACT:
+                assert np.array_equal(got.view(np.uint32), want.view(np.uint32)), G
+            else:
+                assert north_star_ok(got, unf, bound), G
+    da.close()

@@ -33,7 +33,7 @@ def main():
         peak = json.load(open(os.path.join(os.path.dirname(__file__), "..", "MEASURED_PEAKS.json")))["hbm_gbs"]
     except Exception:
         pass
-    ctx = Context(0, torch.cuda.current_stream().cuda_stream)
+    ctx = Context.on_torch_stream(0)
     for name in args.configs:
         t0 = time.time()
         a, x, spec = W.make_config(name, device="cuda", scale_override=args.scale, m_override=args.m)

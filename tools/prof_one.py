@@ -8,7 +8,7 @@ from paper_2312_05639_b200.binding import Context, EXACT_ORDER, NO_COOP
 name, strat, mode = sys.argv[1], sys.argv[2], sys.argv[3]
 iters = int(sys.argv[4]) if len(sys.argv) > 4 and not sys.argv[4].startswith("--") else 5
 scale = int(sys.argv[sys.argv.index("--scale") + 1]) if "--scale" in sys.argv else None
-ctx = Context(0, torch.cuda.current_stream().cuda_stream)
+ctx = Context.on_torch_stream(0)
 a, x, spec = W.make_config(name, device="cuda", scale_override=scale)
 da = ctx.csr_wrap(a)
 y = torch.empty(a.m, spec["d"], device="cuda")
