@@ -74,7 +74,10 @@ int spmx_abi_version(void);
 uint64_t spmx_kernel_launch_count(void);
 
 /* ---- context ------------------------------------------------------------------------ */
-/* `stream` is a cudaStream_t to run on (borrowed), or NULL to create a private one. */
+/* `stream` is a cudaStream_t to run on (borrowed), or NULL to create a private one
+ * (cudaStreamNonBlocking: not ordered with the legacy default stream, whose handle is also
+ * NULL — a caller whose other work runs on the default stream passes an explicit stream or
+ * synchronises before handing device buffers over). */
 int spmx_ctx_create(int device, void* stream, spmx_ctx** out);
 int spmx_ctx_destroy(spmx_ctx* ctx);
 int spmx_ctx_synchronize(spmx_ctx* ctx);
