@@ -732,7 +732,9 @@ __device__ __forceinline__ VecT<VEC> chain_sum(const float* __restrict__ src_c, 
 // lanes (a power of two, <= 32) to every entry of short_list: lane lg sums columns lg*VEC ..
 // of the short chain closed by that boundary, in CSR order. Both orders are fixed by the
 // plan, so the result is deterministic. Only chains closed by a boundary t+1 with t in
-// [t_begin, t_end) are handled (the host pipeline runs the fix-up block by block).
+// [t_begin, t_end) and starting in a chunk in [first_lo, first_hi) are handled: the host
+// pipeline runs the fix-up block by block, and defers the one chain per block whose first
+// partials belong to a block it has not computed yet.
 constexpr int kFixupThreads = 256;
 
 template <int VEC>
@@ -740,6 +742,7 @@ __global__ void __launch_bounds__(kFixupThreads)
 carry_fixup_kernel(const u32* __restrict__ chain_first, const u64* __restrict__ chunk_row,
                    const u32* __restrict__ long_list, u32 n_long,
                    const u32* __restrict__ short_list, u32 n_short, u64 t_begin, u64 t_end,
+                   u64 first_lo, u64 first_hi,
                    const float* __restrict__ carry_out, float* __restrict__ y, int ldx, int c0,
                    int dw, int lpc) {
   if (blockIdx.x < n_long) {
@@ -747,6 +750,7 @@ carry_fixup_kernel(const u32* __restrict__ chain_first, const u64* __restrict__ 
     const u64 last = long_list[blockIdx.x];
     if (last < t_begin || last >= t_end) return;  // CTA-uniform
     const u64 first = __ldg(chain_first + last), rr = __ldg(chunk_row + last + 1);
+    if (first < first_lo || first >= first_hi) return;  // CTA-uniform
     asm volatile("griddepcontrol.wait;" ::: "memory");  // plan data above, SpMM results below
     const int nseg = kFixupThreads / lpc, seg = threadIdx.x / lpc, lg = threadIdx.x % lpc;
     const u64 per = (last - first + nseg) / nseg;  // ceil(len / nseg)
@@ -780,6 +784,7 @@ carry_fixup_kernel(const u32* __restrict__ chain_first, const u64* __restrict__ 
   const u64 last = __ldg(short_list + entry);
   if (last < t_begin || last >= t_end) return;
   const u32 u0 = __ldg(chain_first + last);
+  if (u0 < first_lo || u0 >= first_hi) return;
   const u64 rr = __ldg(chunk_row + last + 1);
   asm volatile("griddepcontrol.wait;" ::: "memory");  // plan data above, SpMM results below
   for (int c = lg * VEC; c < dw; c += lpc * VEC) {
