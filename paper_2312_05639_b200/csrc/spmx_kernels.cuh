@@ -310,10 +310,13 @@ struct Window {
 // window-local row index (kCarryIdx for the row the piece ends in: its partial goes to carry_out).
 constexpr u32 kCarryIdx = 0xffffffffu;
 // Column indices and values reach the lanes of a group through shared memory where a group is
-// 8 lanes (the precompiled widths): every lane publishes the pair (column of position t + U,
-// value of position t) of its position once per batch, and each position is one LDS.64 —
-// half the instructions and L1 data-pipe wavefronts of two shuffles per position (shuffles
-// go through the same pipe as the gathers: at d = 32 they were a third of its load).
+// 8 lanes and the gather pipeline is as deep as a batch (U == G: d = 32 and 64): every lane
+// publishes the pair (column of position t + U, value of position t) of its position once per
+// batch, and each position is one LDS.64 — half the instructions and L1 data-pipe wavefronts
+// of two shuffles per position (shuffles go through the same pipe as the gathers: at d = 32
+// they were a third of its load). With U < G (d = 128) the column belongs to a gather issued
+// G - U positions later; the variant with that column queue ran 6 % slower (registers), so
+// those kernels keep the shuffles.
 #ifndef SPMX_SMEM_BCAST
 #define SPMX_SMEM_BCAST 1
 #endif
