@@ -29,6 +29,8 @@ import sys
 
 _INSTR = re.compile(r"\s+/\*([0-9a-f]{4,})\*/\s+(.*?);\s+/\* (0x[0-9a-f]{16}) \*/")
 _HI = re.compile(r"\s+/\* (0x[0-9a-f]{16}) \*/")
+# a row gather of the walk loop: 128-bit load through the read-only path
+_GATHER = re.compile(r"LDG\.E(\.\w+)*\.128\.CONSTANT")
 # branch with its target (plain, predicated, or uniform: "BRA.U !UP0, 0x23b0")
 _BRA = r"\bBRA(?:\.U)?\s+(?:!?UP\d+,\s*)?(0x[0-9a-f]+)"
 
@@ -174,7 +176,7 @@ def plan_patch(code, log=None):
         top = next((j for j, c in enumerate(code) if c.addr == tgt), None)
         if top is None:
             continue
-        n = sum(1 for c in code[top:i] if "LDG.E.128.CONSTANT" in c.text)
+        n = sum(1 for c in code[top:i] if _GATHER.search(c.text))
         inner = any(re.search(_BRA, c.text) and
                     int(re.search(_BRA, c.text).group(1), 16) < c.addr for c in code[top:i])
         if n >= 4 and not inner and (best is None or n > best[2]):
@@ -184,7 +186,7 @@ def plan_patch(code, log=None):
         return None
     top, end, n_ld = best
     body = code[top:end + 1]
-    loads = [k for k, c in enumerate(body) if "LDG.E.128.CONSTANT" in c.text]
+    loads = [k for k, c in enumerate(body) if _GATHER.search(c.text)]
     if any(body[k].wb != 5 for k in loads):
         say("gathers are not all on SB5")
         return None
