@@ -58,7 +58,6 @@ extern "C" {
                                than 16 pieces: 16 runs of consecutive pieces, then the runs) —
                                deterministic, within the north_star tolerance; all other rows stay
                                bitwise equal. */
-#define SPMX_NO_COOP 2u     /* reserved (no effect) */
 #define SPMX_JIT_WIDTH 4u   /* instantiate the kernel for exactly this d at run time (NVRTC, cached
                                per d and device) instead of using the runtime-d kernels: the GPU
                                counterpart of the reference's per-d code generation
@@ -70,6 +69,9 @@ typedef struct spmx_plan spmx_plan; /* partition of A for one (strategy, parts, 
 
 const char* spmx_last_error(void);
 int spmx_abi_version(void);
+/* "key=value;" pairs describing the loaded build: SPMX_SASS_SCHED=<n> (kernels whose gather
+ * pipeline was re-scheduled after linking, 0 = as compiled), cuda=<CUDART_VERSION>, arch. */
+const char* spmx_build_info(void);
 /* number of kernels this library has launched on the calling process (all contexts) */
 uint64_t spmx_kernel_launch_count(void);
 
@@ -100,6 +102,11 @@ int spmx_csr_upload(spmx_ctx* ctx, int64_t m, int64_t n, int64_t nnz, const uint
 int spmx_csr_wrap_device(spmx_ctx* ctx, int64_t m, int64_t n, int64_t nnz,
                          const uint64_t* d_row_ptr, const uint32_t* d_col_indices,
                          const float* d_vals, int validate, spmx_csr** out);
+/* structure only: row_ptr without columns or values. Enough for the partitioner and for
+ * spmx_plan_create (neither reads col_indices / vals: partition.cpp:35-84 only touches row_ptr);
+ * spmx_spmm on such a handle is SPMX_ELOGIC. */
+int spmx_rowptr_upload(spmx_ctx* ctx, int64_t m, int64_t nnz, const uint64_t* row_ptr,
+                       spmx_csr** out);
 int spmx_csr_destroy(spmx_csr* a);
 int spmx_csr_dims(const spmx_csr* a, int64_t* m, int64_t* n, int64_t* nnz);
 
@@ -173,6 +180,93 @@ int spmx_jit_available(void);
 /* checksum(Y), dense.cpp:17-28, of a device buffer (FNV-1a is sequential: the buffer is copied
  * to the host and hashed there; a reporting helper, not on the hot path) */
 int spmx_checksum_device(spmx_ctx* ctx, const float* d_y, size_t count, uint64_t* out);
+
+/* ---- multi-GPU driver (north_star item 3) ------------------------------------
+ * The reference parallelises ONE way: contiguous row ranges of A, one per worker, joined by a
+ * barrier (fork-join over RowRanges, executor.cpp:66-99; single writer per output row,
+ * SPEC.md:439). The driver applies the same division one level up: A is cut into G row blocks
+ * ("shards") by the reference's own split_nnz(A, G) (partition.cpp:35-51; split_merge(A, G),
+ * partition.cpp:69-84, on request), computed by the device partitioner and therefore bit-exact
+ * with it; shard g lives on one GPU with a rebased row_ptr; X is replicated by ONE NCCL
+ * broadcast; every GPU multiplies its shards with its own plan (the chosen Strategy divides the
+ * shard again among the SMs); Y stays row-sharded. No collective is on the data path. An
+ * all-gather-v of Y (one ncclBroadcast per shard inside one NCCL group, no padding) is offered
+ * and timed separately.
+ *
+ * Two ways to build the communicator:
+ *   spmx_mg_create       one process drives n_devices GPUs (ncclCommInitAll), one context and
+ *                        stream per GPU — the C++ mirror's RunConfig.gpus and the CLI's --gpus;
+ *   spmx_mg_create_rank  one process per GPU (torchrun / mpirun): rank `rank` of `world`, the
+ *                        128-byte id made by spmx_mg_unique_id on rank 0 and handed to the
+ *                        other ranks by the launcher. id128 == NULL builds the driver without a
+ *                        communicator (world must then be served by another transport: only
+ *                        the shard / plan / spmm calls work; used to exercise the rank code
+ *                        path with several processes on one GPU).
+ * n_shards == 0 means one shard per rank; n_shards > world puts several shards on a rank
+ * (shard g on rank g * world / n_shards, run back to back on that rank's stream), which lets one
+ * GPU stand in for a node in the tests. NCCL is loaded with dlopen (SPMX_NCCL_LIB, then
+ * libnccl.so.2): the library has no link-time dependency on it, and the single-GPU entry
+ * points above never touch it. Every rank calls every spmx_mg_* function with the same
+ * arguments (its own copy of A's arrays), like any SPMD collective API. */
+typedef struct spmx_mg spmx_mg;
+
+#define SPMX_SHARD_BY_NNZ 1   /* split_nnz(A, G): equal nonzeros per shard (north_star) */
+#define SPMX_SHARD_BY_MERGE 2 /* split_merge(A, G): equal rows + nonzeros per shard */
+
+int spmx_mg_create(int n_devices, const int* devices, int n_shards, spmx_mg** out);
+int spmx_mg_unique_id(void* out128);
+int spmx_mg_create_rank(int device, void* stream, int rank, int world, int n_shards,
+                        const void* id128, spmx_mg** out);
+int spmx_mg_destroy(spmx_mg* mg);
+/* world size, ranks driven by this process, shards in total / on this process, NCCL version
+ * (0 without a communicator); any pointer may be NULL */
+int spmx_mg_info(const spmx_mg* mg, int* world, int* n_local_ranks, int* n_shards,
+                 int* n_local_shards, int* nccl_version);
+/* pure host function: the rank that owns shard g (g * world / n_shards) */
+int spmx_mg_shard_owner(int n_shards, int world, int shard);
+
+/* Cut A into the driver's shards and place every LOCAL shard on its GPU. *_host reads the
+ * reference's host arrays (CsrMatrix fields, csr.hpp:10-20): row_ptr goes to the first local GPU
+ * once (structure only), col/vals slices go straight to their owners. *_device takes arrays
+ * that already live on local rank `src_local_rank`'s GPU (copied device to device / peer to
+ * peer). out_ranges (2 * n_shards, may be NULL) receives ALL shards' row ranges, which are
+ * bit-exact with split_nnz / split_merge of the reference. Replaces any earlier sharding. */
+int spmx_mg_shard_host(spmx_mg* mg, int64_t m, int64_t n, int64_t nnz, const uint64_t* row_ptr,
+                       const uint32_t* col_indices, const float* vals, int shard_by,
+                       uint64_t* out_ranges);
+int spmx_mg_shard_device(spmx_mg* mg, int src_local_rank, int64_t m, int64_t n, int64_t nnz,
+                         const uint64_t* d_row_ptr, const uint32_t* d_col_indices,
+                         const float* d_vals, int shard_by, uint64_t* out_ranges);
+/* local shard i: its global index, the device it lives on, its rows [begin, end) of A and nnz */
+int spmx_mg_shard_info(const spmx_mg* mg, int local_shard, int* global_shard, int* device,
+                       uint64_t* row_begin, uint64_t* row_end, uint64_t* nnz);
+
+/* make_partition per shard (spmx_plan_create on every local shard) */
+int spmx_mg_plan(spmx_mg* mg, int strategy, unsigned parts, int dynamic, uint64_t batch,
+                 unsigned flags);
+
+/* X (x_rows x d) to every GPU with ONE ncclBroadcast from rank root_rank, timed with CUDA events
+ * (max over this process's ranks). *_host: the process that drives root_rank passes its host
+ * matrix (uploaded to the root GPU first, h2d_ms), the driver owns the device copies.
+ * *_device: d_x_local[i] is local rank i's x_rows x d buffer (borrowed; the root's holds X). */
+int spmx_mg_broadcast_x_host(spmx_mg* mg, const float* x_host, int root_rank, int64_t x_rows,
+                             int64_t d, float* h2d_ms, float* bcast_ms);
+int spmx_mg_broadcast_x_device(spmx_mg* mg, float* const* d_x_local, int root_rank,
+                               int64_t x_rows, int64_t d, float* bcast_ms);
+
+/* Y_g = A_g * X on every local shard (run_spmm's parallel region, executor.cpp:70-97, with
+ * GPUs for threads). step_ms = max over this process's ranks of the device time of that rank's
+ * shards (CUDA events on the rank's stream); ms_per_local_shard (may be NULL) gets each
+ * shard's own time. The ranks never wait for each other. */
+int spmx_mg_spmm(spmx_mg* mg, float* step_ms, float* ms_per_local_shard);
+/* device pointer of local shard i's Y block ((row_end - row_begin) x d, owned by the driver) */
+int spmx_mg_y_shard(const spmx_mg* mg, int local_shard, float** d_y);
+/* the local shards' rows of Y into a host M x d matrix (other rows are left untouched) */
+int spmx_mg_download_y(spmx_mg* mg, float* y_host);
+/* optional: the full M x d Y on every GPU, one ncclBroadcast per shard in one group
+ * (all-gather-v: shards have unequal row counts, nothing is padded) */
+int spmx_mg_allgather_y(spmx_mg* mg, float* elapsed_ms);
+int spmx_mg_y_full(const spmx_mg* mg, int local_rank, float** d_y_full);
 
 #ifdef __cplusplus
 }

@@ -9,6 +9,7 @@ from __future__ import annotations
 
 import ctypes as C
 import os
+import shutil
 import subprocess
 import sys
 
@@ -18,13 +19,13 @@ _PKG = os.path.dirname(os.path.abspath(__file__))
 _ROOT = os.path.dirname(_PKG)
 # SPMX_B200_LIB selects another build of the same library (kernel-tuning experiments only)
 LIB_PATH = os.environ.get("SPMX_B200_LIB") or os.path.join(_PKG, "libspmx_b200.so")
+ASBUILT_PATH = os.path.splitext(LIB_PATH)[0] + "_asbuilt.so"
 CSRC = os.path.join(_PKG, "csrc")
 HEADER = os.path.join(_ROOT, "include", "spmx_b200.h")
 
 ROW, NNZ, MERGE = 0, 1, 2
 STRATEGY = {"row": ROW, "nnz": NNZ, "merge": MERGE}
 EXACT_ORDER = 1
-NO_COOP = 2
 JIT_WIDTH = 4
 
 NVCC_FLAGS = ["-gencode", "arch=compute_100a,code=sm_100a", "-lineinfo", "-O3", "-std=c++17",
@@ -70,12 +71,17 @@ def build_library(force: bool = False, verbose: bool = False) -> str:
     if verbose:
         print(" ".join(cmd), file=sys.stderr)
     subprocess.check_call(cmd)
+    # the library exactly as nvcc linked it, kept beside the shipped one for the A/B parity test
+    # of the post-link step (tests/test_sass_ab_gpu.py); nothing else loads it
+    shutil.copyfile(LIB_PATH, ASBUILT_PATH)
     # second scoreboard for half of the walk loop's gathers (sass_sched.py):
     # applied only when its preconditions hold, SPMX_NO_SASS_SCHED=1 leaves the kernels as compiled
     if not os.environ.get("SPMX_NO_SASS_SCHED"):
         from . import sass_sched
         say = (lambda m: print("sass_sched:", m, file=sys.stderr)) if verbose else (lambda m: None)
-        n = sass_sched.patch_library(LIB_PATH, log=say)
+        # strict: a precompiled width whose preconditions fail stops the build (a silent
+        # fall-back to the compiled schedule would ship a 5-13 % slower kernel unnoticed)
+        n = sass_sched.patch_library(LIB_PATH, log=say, strict=True)
         say(f"{n} kernel(s) re-scheduled")
     return LIB_PATH
 
@@ -98,16 +104,19 @@ class Lib:
             cls._inst = cls()
         return cls._inst
 
-    def __init__(self):
-        if not os.path.exists(LIB_PATH):
+    def __init__(self, path: str | None = None):
+        path = path or LIB_PATH
+        if not os.path.exists(path):
             raise FileNotFoundError(
-                f"{LIB_PATH} is missing: build it with `python -c 'import __graft_entry__ as g; "
+                f"{path} is missing: build it with `python -c 'import __graft_entry__ as g; "
                 f"g.build()'` — there is no CPU fallback for this path")
-        L = self.lib = C.CDLL(LIB_PATH)
+        self.path = path
+        L = self.lib = C.CDLL(path)
         vp, i64, u64, sz = C.c_void_p, C.c_int64, C.c_uint64, C.c_size_t
         P = C.POINTER
         L.spmx_last_error.restype = C.c_char_p
         L.spmx_abi_version.restype = C.c_int
+        L.spmx_build_info.restype = C.c_char_p
         L.spmx_kernel_launch_count.restype = u64
         L.spmx_ctx_create.argtypes = [C.c_int, vp, P(vp)]
         L.spmx_ctx_destroy.argtypes = [vp]
@@ -121,6 +130,7 @@ class Lib:
         L.spmx_host_free_pinned.argtypes = [vp]
         L.spmx_csr_upload.argtypes = [vp, i64, i64, i64, vp, vp, vp, P(vp)]
         L.spmx_csr_wrap_device.argtypes = [vp, i64, i64, i64, vp, vp, vp, C.c_int, P(vp)]
+        L.spmx_rowptr_upload.argtypes = [vp, i64, i64, vp, P(vp)]
         L.spmx_csr_destroy.argtypes = [vp]
         L.spmx_csr_dims.argtypes = [vp, P(i64), P(i64), P(i64)]
         L.spmx_split_rows_static.argtypes = [vp, u64, C.c_uint, vp]
@@ -154,6 +164,11 @@ class Lib:
         self.lib.spmx_jit_stats(C.byref(n), C.byref(t))
         return n.value, t.value
 
+    def build_info(self) -> dict:
+        """{'SPMX_SASS_SCHED': '6', 'cuda': '12090', ...} of the loaded library."""
+        txt = self.lib.spmx_build_info().decode()
+        return dict(kv.split("=", 1) for kv in txt.split(";") if "=" in kv)
+
     def launch_count(self) -> int:
         return int(self.lib.spmx_kernel_launch_count())
 
@@ -173,8 +188,8 @@ class Context:
     """spmx_ctx: one (device, stream). stream=None creates a private stream; pass a torch
     stream's .cuda_stream to run on it."""
 
-    def __init__(self, device: int = 0, stream: int | None = None):
-        self.L = Lib.get()
+    def __init__(self, device: int = 0, stream: int | None = None, lib: "Lib | None" = None):
+        self.L = lib or Lib.get()
         h = C.c_void_p()
         self.L.check(self.L.lib.spmx_ctx_create(device, C.c_void_p(stream or 0), C.byref(h)))
         self.h = h
@@ -232,6 +247,15 @@ class Context:
         self.L.check(self.L.lib.spmx_csr_upload(self.h, m, n, nnz, _ptr(rp), _ptr(col) if col.size else 0,
                                                 _ptr(vals) if vals.size else 0, C.byref(h)))
         return DeviceCsr(self, h, m, n, nnz)
+
+    def rowptr_upload(self, m, row_ptr, nnz=None) -> "DeviceCsr":
+        """Structure-only handle (partitioner and plan input)."""
+        rp = _np_u64(row_ptr)
+        if nnz is None:
+            nnz = int(rp[m]) if rp.size > m else -1
+        h = C.c_void_p()
+        self.L.check(self.L.lib.spmx_rowptr_upload(self.h, m, nnz, _ptr(rp), C.byref(h)))
+        return DeviceCsr(self, h, m, 0, nnz)
 
     def csr_wrap(self, csr, validate=True) -> "DeviceCsr":
         """Borrow a workloads.Csr whose tensors already live on this device."""

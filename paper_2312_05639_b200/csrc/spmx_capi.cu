@@ -25,7 +25,16 @@
 
 using spmx_dev::u64;
 
+#define SPMX_STR2(x) #x
+#define SPMX_STR(x) SPMX_STR2(x)
+
 namespace {
+
+// "key=value;" pairs. The digit after SPMX_SASS_SCHED= is rewritten in the linked library by
+// the post-link scheduling step (sass_sched.py): the number of kernels it re-scheduled, 0 when
+// the library runs the schedule exactly as ptxas emitted it. Kept in writable data so that the
+// text exists once in the binary.
+char g_build_info[96] = "SPMX_SASS_SCHED=0;" "cuda=" SPMX_STR(CUDART_VERSION) ";arch=sm_100a;";
 
 thread_local std::string g_last_error;
 std::atomic<uint64_t> g_launches{0};
@@ -108,6 +117,7 @@ struct spmx_csr {
   uint32_t* col = nullptr;
   float* vals = nullptr;
   bool owned = false;
+  bool structure_only = false;  // spmx_rowptr_upload: partitioner / plan input only
 };
 
 struct spmx_plan {
@@ -173,6 +183,25 @@ void dev_free_async(spmx_ctx* ctx, void* p) {
   if (p) cudaFreeAsync(p, ctx->stream);
 }
 
+// Temporaries of a plan build / partition call: returned to the stream-ordered pool when the
+// scope is left, on the exception path as well.
+struct AsyncScratch {
+  spmx_ctx* ctx;
+  std::vector<void*> ptrs;
+  explicit AsyncScratch(spmx_ctx* c) : ctx(c) {}
+  AsyncScratch(const AsyncScratch&) = delete;
+  AsyncScratch& operator=(const AsyncScratch&) = delete;
+  template <typename T>
+  T* get(size_t count) {
+    T* p = dev_alloc_async<T>(ctx, count);
+    ptrs.push_back(p);
+    return p;
+  }
+  ~AsyncScratch() {
+    for (void* p : ptrs) dev_free_async(ctx, p);
+  }
+};
+
 void launched(unsigned n = 1) { g_launches.fetch_add(n, std::memory_order_relaxed); }
 
 void post_launch() {
@@ -204,14 +233,14 @@ void strategy_row_boundaries(spmx_ctx* ctx, const spmx_csr* a, int strategy, uns
 }
 
 void ranges_to_host(spmx_ctx* ctx, const u64* d_bnd, unsigned parts, uint64_t* out) {
-  u64* d_ranges = dev_alloc<u64>(2 * (size_t)parts);
+  AsyncScratch tmp(ctx);
+  u64* d_ranges = tmp.get<u64>(2 * (size_t)parts);
   spmx_dev::ranges_from_boundaries_kernel<<<blocks_for(parts), 256, 0, ctx->stream>>>(
       d_bnd, parts, d_ranges);
   post_launch();
   CUDA_CHECK(cudaMemcpyAsync(out, d_ranges, 2 * (size_t)parts * sizeof(u64),
                              cudaMemcpyDeviceToHost, ctx->stream));
   CUDA_CHECK(cudaStreamSynchronize(ctx->stream));
-  CUDA_CHECK(cudaFree(d_ranges));
 }
 
 const char* csr_error_text(int err) {
@@ -485,7 +514,10 @@ spmx_plan* plan_build(spmx_ctx* ctx, const spmx_csr* a, int strategy, unsigned p
     const u64 want = exact ? fine : std::min<u64>(fine, (u64)ctx->sm_count * default_parts_per_sm());
     parts = (unsigned)std::min<u64>(std::max<u64>(want, 1), 1u << 30);
   }
+  if (dynamic && nnz >= (1ull << 32))
+    throw InvalidArg("dynamic dispatch: a claimed row batch must span fewer than 2^32 nonzeros");
   spmx_plan* p = new spmx_plan;
+  AsyncScratch tmp(ctx);  // freed on every way out
   try {
     p->ctx = ctx;
     p->csr = a;
@@ -500,14 +532,14 @@ spmx_plan* plan_build(spmx_ctx* ctx, const spmx_csr* a, int strategy, unsigned p
       return p;
     }
     // 1. the strategy's row-snapped boundaries and RowRange list (bit-exact with the reference)
-    u64* d_bnd = dev_alloc_async<u64>(ctx, (size_t)parts + 1);
+    u64* d_bnd = tmp.get<u64>((size_t)parts + 1);
     strategy_row_boundaries(ctx, a, strategy, parts, d_bnd);
     p->ranges = dev_alloc_async<u64>(ctx, 2 * (size_t)parts);
     spmx_dev::ranges_from_boundaries_kernel<<<blocks_for(parts), 256, 0, ctx->stream>>>(
         d_bnd, parts, p->ranges);
     post_launch();
     // 2. strategy-level merge-path diagonals
-    u64* d_diag = dev_alloc_async<u64>(ctx, (size_t)parts + 1);
+    u64* d_diag = tmp.get<u64>((size_t)parts + 1);
     if (strategy == SPMX_MERGE_SPLIT && !exact) {
       spmx_dev::merge_boundaries_kernel<<<blocks_for((u64)parts + 1), 256, 0, ctx->stream>>>(
           a->row_ptr, m, nnz, parts, 0, d_diag);
@@ -527,8 +559,8 @@ spmx_plan* plan_build(spmx_ctx* ctx, const spmx_csr* a, int strategy, unsigned p
           a->row_ptr, m, nnz, d_diag, p->n_chunks + 1, p->chunk_row, p->chunk_nnz);
       post_launch();
     } else {
-      u64* d_cnt = dev_alloc_async<u64>(ctx, parts);
-      u64* d_off = dev_alloc_async<u64>(ctx, (size_t)parts + 1);
+      u64* d_cnt = tmp.get<u64>(parts);
+      u64* d_off = tmp.get<u64>((size_t)parts + 1);
       // Tail taper: the last wave of the grid is cut into half-size chunks and its last third
       // into quarter-size chunks, so that the SMs run dry together (one wave = the chunks
       // resident at once, 64 per SM).
@@ -571,8 +603,6 @@ spmx_plan* plan_build(spmx_ctx* ctx, const spmx_csr* a, int strategy, unsigned p
       CUDA_CHECK(cudaMemcpyAsync(&p->n_short, p->short_buf, sizeof(uint32_t), cudaMemcpyDeviceToHost,
                                  ctx->stream));
       CUDA_CHECK(cudaStreamSynchronize(ctx->stream));
-      dev_free_async(ctx, d_cnt);
-      dev_free_async(ctx, d_off);
       // a piece ends inside a row only where a chain of carries exists: without chains no
       // carry is ever written and the fix-up has nothing to do
       p->may_carry = p->n_long + p->n_short > 0;
@@ -584,9 +614,20 @@ spmx_plan* plan_build(spmx_ctx* ctx, const spmx_csr* a, int strategy, unsigned p
               p->chunk_row, p->chunk_nnz, p->n_chunks, p->work);
       post_launch();
     }
+    // a work item's nonzero offsets are 32-bit inside the kernel: every chunk must span fewer
+    // than 2^32 nonzeros (only exact-order plans, one chunk per strategy range, can exceed it)
+    u64 max_span = 0;
+    if (p->n_chunks > 0 && nnz >= (1ull << 32)) {
+      u64* d_max = tmp.get<u64>(1);
+      CUDA_CHECK(cudaMemsetAsync(d_max, 0, sizeof(u64), ctx->stream));
+      spmx_dev::max_chunk_span_kernel<<<blocks_for(p->n_chunks), 256, 0, ctx->stream>>>(
+          p->chunk_nnz, p->n_chunks, d_max);
+      post_launch();
+      CUDA_CHECK(cudaMemcpyAsync(&max_span, d_max, sizeof(u64), cudaMemcpyDeviceToHost, ctx->stream));
+    }
     CUDA_CHECK(cudaStreamSynchronize(ctx->stream));
-    dev_free_async(ctx, d_diag);
-    dev_free_async(ctx, d_bnd);
+    if (max_span >= (1ull << 32))
+      throw InvalidArg("plan: a range spans 2^32 or more nonzeros (use more parts)");
     return p;
   } catch (...) {
     plan_free(p);
@@ -610,7 +651,8 @@ void* ws_get(spmx_ctx* ctx, int slot, size_t bytes) {
 extern "C" {
 
 const char* spmx_last_error(void) { return g_last_error.c_str(); }
-int spmx_abi_version(void) { return 1; }
+int spmx_abi_version(void) { return 2; }
+const char* spmx_build_info(void) { return g_build_info; }
 uint64_t spmx_kernel_launch_count(void) { return g_launches.load(); }
 
 int spmx_ctx_create(int device, void* stream, spmx_ctx** out) {
@@ -735,6 +777,40 @@ int spmx_csr_upload(spmx_ctx* ctx, int64_t m, int64_t n, int64_t nnz, const uint
   });
 }
 
+int spmx_rowptr_upload(spmx_ctx* ctx, int64_t m, int64_t nnz, const uint64_t* row_ptr,
+                       spmx_csr** out) {
+  return guarded([&] {
+    check(ctx);
+    if (!out) throw InvalidArg("spmx_rowptr_upload: null out");
+    if (m < 0 || nnz < 0) throw InvalidArg("invalid CSR: negative dimension");
+    if (!row_ptr) throw InvalidArg("invalid CSR: null array");
+    spmx_csr* a = new spmx_csr;
+    a->ctx = ctx;
+    a->m = m;
+    a->n = 0;
+    a->nnz = nnz;
+    a->owned = true;
+    a->structure_only = true;
+    try {
+      a->row_ptr = dev_alloc<u64>((size_t)m + 1);
+      CUDA_CHECK(cudaMemcpyAsync(a->row_ptr, row_ptr, ((size_t)m + 1) * 8, cudaMemcpyHostToDevice,
+                                 ctx->stream));
+      CUDA_CHECK(cudaMemsetAsync(ctx->d_err, 0, sizeof(int), ctx->stream));
+      spmx_dev::validate_row_ptr_kernel<<<validate_grid(ctx, (u64)m), 256, 0, ctx->stream>>>(
+          a->row_ptr, (u64)m, (u64)nnz, ctx->d_err);
+      post_launch();
+      int err = 0;
+      CUDA_CHECK(cudaMemcpyAsync(&err, ctx->d_err, sizeof(int), cudaMemcpyDeviceToHost, ctx->stream));
+      CUDA_CHECK(cudaStreamSynchronize(ctx->stream));
+      if (err) throw InvalidArg(std::string("invalid CSR: ") + csr_error_text(err));
+    } catch (...) {
+      spmx_csr_destroy(a);
+      throw;
+    }
+    *out = a;
+  });
+}
+
 int spmx_csr_wrap_device(spmx_ctx* ctx, int64_t m, int64_t n, int64_t nnz, const uint64_t* d_rp,
                          const uint32_t* d_col, const float* d_vals, int validate,
                          spmx_csr** out) {
@@ -788,12 +864,12 @@ int spmx_split_rows_static(spmx_ctx* ctx, uint64_t m, unsigned parts, uint64_t* 
   return guarded([&] {
     check(ctx);
     if (parts == 0) throw InvalidArg("split_rows_static: zero threads");
-    u64* d_bnd = dev_alloc<u64>((size_t)parts + 1);
+    AsyncScratch tmp(ctx);
+    u64* d_bnd = tmp.get<u64>((size_t)parts + 1);
     spmx_dev::row_boundaries_kernel<<<blocks_for((u64)parts + 1), 256, 0, ctx->stream>>>(
         (u64)m, parts, d_bnd);
     post_launch();
     ranges_to_host(ctx, d_bnd, parts, out);
-    CUDA_CHECK(cudaFree(d_bnd));
   });
 }
 
@@ -802,10 +878,10 @@ int spmx_split_nnz(spmx_ctx* ctx, const spmx_csr* a, unsigned parts, uint64_t* o
     check(ctx);
     check(a);
     if (parts == 0) throw InvalidArg("split_nnz: zero threads");
-    u64* d_bnd = dev_alloc<u64>((size_t)parts + 1);
+    AsyncScratch tmp(ctx);
+    u64* d_bnd = tmp.get<u64>((size_t)parts + 1);
     strategy_row_boundaries(ctx, a, SPMX_NNZ_SPLIT, parts, d_bnd);
     ranges_to_host(ctx, d_bnd, parts, out);
-    CUDA_CHECK(cudaFree(d_bnd));
   });
 }
 
@@ -814,10 +890,10 @@ int spmx_split_merge(spmx_ctx* ctx, const spmx_csr* a, unsigned parts, uint64_t*
     check(ctx);
     check(a);
     if (parts == 0) throw InvalidArg("split_merge: zero threads");
-    u64* d_bnd = dev_alloc<u64>((size_t)parts + 1);
+    AsyncScratch tmp(ctx);
+    u64* d_bnd = tmp.get<u64>((size_t)parts + 1);
     strategy_row_boundaries(ctx, a, SPMX_MERGE_SPLIT, parts, d_bnd);
     ranges_to_host(ctx, d_bnd, parts, out);
-    CUDA_CHECK(cudaFree(d_bnd));
   });
 }
 
@@ -924,6 +1000,7 @@ int spmx_spmm(spmx_ctx* ctx, const spmx_plan* plan, const spmx_csr* a, const flo
     check(a);
     if (plan->csr != a || plan->ctx != ctx)
       throw LogicErr("spmx_spmm: plan was built for another matrix or context");
+    if (a->structure_only) throw LogicErr("spmx_spmm: structure-only CSR handle (spmx_rowptr_upload)");
     if (a->n != x_rows) throw InvalidArg("run_spmm: A.n != X.rows");  // executor.cpp:38
     if (d < 1) throw InvalidArg("run_spmm: X.cols must be >= 1");
     if (d > (1 << 30)) throw InvalidArg("run_spmm: X.cols too large");
@@ -1123,6 +1200,7 @@ int spmx_spmm_reference(spmx_ctx* ctx, const spmx_csr* a, const float* d_x, int6
   return guarded([&] {
     check(ctx);
     check(a);
+    if (a->structure_only) throw LogicErr("spmm_reference: structure-only CSR handle");
     if (a->n != x_rows) throw InvalidArg("spmm_reference: A.n != X.rows");  // reference.cpp:11
     if (d < 1) throw InvalidArg("spmm_reference: X.cols must be >= 1");
     const u64 total = (u64)a->m * (u64)d;

@@ -383,6 +383,15 @@ __device__ __forceinline__ void process_piece(const SpmmArgs& a, bool active, u6
   const float zero_f = __int_as_float(a.dw >> 31);  // 0.0f (dw >= 0), opaque to the compiler
   const u64 pol_first = policy_evict_first(), pol_last = policy_evict_last();
 
+  // A piece without nonzeros that ends inside row r1 (duplicate diagonals: more parts than
+  // merge items) still owns a slot of that row's carry chain: its partial is zero. Without
+  // this store carry_fixup_kernel would add whatever the buffer held before.
+  if (carry_lane != nullptr && active && span == 0u && r1 < a.m) {
+    float z[NT][VEC];
+    zero_acc(z);
+    store_lane<G, VEC, NT, RAGGED>(a, carry_lane, lg, z, pol_first);
+  }
+
   u32 ws = 0;  // nonzero offset where the current window starts
   int adv = 0;  // rows the previous window covered
   for (u64 wbase = r0; __any_sync(kFullMask, wbase < row_lim); wbase += adv) {
@@ -624,6 +633,8 @@ spmm_dynamic_kernel(const SpmmArgs a) {
   constexpr int NGW = 32 / G;
   __shared__ WarpScratch<G> scratch[kWarpsPerCta];
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5, g = lane / G;
+  // invalid input found by the validation kernels ahead of this launch: gather nothing
+  if (a.abort_flag && *(volatile const int*)a.abort_flag) return;
   u64 v = 0;
   if (lane == 0) v = atomicAdd(a.counter, a.batch);
   v = __shfl_sync(kFullMask, v, 0);
@@ -748,13 +759,19 @@ carry_fixup_kernel(const u32* __restrict__ chain_first, const u64* __restrict__ 
                    u64 first_lo, u64 first_hi,
                    const float* __restrict__ carry_out, float* __restrict__ y, int ldx, int c0,
                    int dw, int lpc) {
+  // Launched with programmatic stream serialisation: EVERY thread executes griddepcontrol.wait
+  // before it retires, also the ones with nothing to do — a grid in which nobody waits could
+  // complete while the SpMM grid before it is still running, and whatever follows on the
+  // stream (the Y download of the host pipeline, the next block's kernels) is ordered after
+  // this grid only. Plan data is read above the wait, SpMM results below it.
   if (blockIdx.x < n_long) {
     __shared__ VecT<VEC> seg_sum[kFixupThreads];
     const u64 last = long_list[blockIdx.x];
-    if (last < t_begin || last >= t_end) return;  // CTA-uniform
-    const u64 first = __ldg(chain_first + last), rr = __ldg(chunk_row + last + 1);
-    if (first < first_lo || first >= first_hi) return;  // CTA-uniform
-    asm volatile("griddepcontrol.wait;" ::: "memory");  // plan data above, SpMM results below
+    const bool mine = last >= t_begin && last < t_end;  // CTA-uniform
+    u64 first = 0, rr = 0;
+    if (mine) { first = __ldg(chain_first + last); rr = __ldg(chunk_row + last + 1); }
+    asm volatile("griddepcontrol.wait;" ::: "memory");
+    if (!mine || first < first_lo || first >= first_hi) return;  // CTA-uniform
     const int nseg = kFixupThreads / lpc, seg = threadIdx.x / lpc, lg = threadIdx.x % lpc;
     const u64 per = (last - first + nseg) / nseg;  // ceil(len / nseg)
     const u64 ub = min(first + (u64)seg * per, last + 1), ue = min(ub + per, last + 1);
@@ -782,14 +799,21 @@ carry_fixup_kernel(const u32* __restrict__ chain_first, const u64* __restrict__ 
   const u64 tid = (u64)(blockIdx.x - n_long) * kFixupThreads + threadIdx.x;
   const u64 entry = tid / (unsigned)lpc;
   const int lg = (int)(tid % (unsigned)lpc);
-  if (entry >= n_short) return;
   // chunk whose END boundary closes this chain
-  const u64 last = __ldg(short_list + entry);
-  if (last < t_begin || last >= t_end) return;
-  const u32 u0 = __ldg(chain_first + last);
-  if (u0 < first_lo || u0 >= first_hi) return;
-  const u64 rr = __ldg(chunk_row + last + 1);
-  asm volatile("griddepcontrol.wait;" ::: "memory");  // plan data above, SpMM results below
+  u64 last = 0, rr = 0;
+  u32 u0 = 0;
+  bool mine = entry < n_short;
+  if (mine) {
+    last = __ldg(short_list + entry);
+    mine = last >= t_begin && last < t_end;
+  }
+  if (mine) {
+    u0 = __ldg(chain_first + last);
+    rr = __ldg(chunk_row + last + 1);
+    mine = u0 >= first_lo && u0 < first_hi;
+  }
+  asm volatile("griddepcontrol.wait;" ::: "memory");
+  if (!mine) return;
   for (int c = lg * VEC; c < dw; c += lpc * VEC) {
     float* dst = y + (size_t)rr * ldx + c0 + c;
     const VecT<VEC> tail = *reinterpret_cast<const VecT<VEC>*>(dst);

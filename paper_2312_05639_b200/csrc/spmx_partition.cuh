@@ -241,6 +241,14 @@ work_items_kernel(const u64* __restrict__ chunk_row, const u64* __restrict__ chu
   }
 }
 
+// Largest nonzero span of a chunk (the kernel keeps nonzero offsets inside a chunk in 32 bits).
+__global__ void max_chunk_span_kernel(const u64* __restrict__ chunk_nnz, u64 n_chunks,
+                                      u64* __restrict__ out) {
+  const u64 c = (u64)blockIdx.x * blockDim.x + threadIdx.x;
+  if (c >= n_chunks) return;
+  atomicMax(out, chunk_nnz[c + 1] - chunk_nnz[c]);
+}
+
 // validate_csr, src/csr.cpp:18-42, on the device. err receives the largest code seen:
 // 2 row_ptr[0] != 0, 3 row_ptr[m] != nnz, 4 row_ptr decreasing, 5 column out of range.
 __global__ void validate_row_ptr_kernel(const u64* __restrict__ row_ptr, u64 m, u64 nnz, int* err) {

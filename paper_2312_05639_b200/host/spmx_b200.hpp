@@ -25,6 +25,7 @@
 #include <algorithm>
 #include <cstdint>
 #include <cstring>
+#include <memory>
 #include <optional>
 #include <stdexcept>
 #include <string>
@@ -92,11 +93,10 @@ struct DevCsr {
     check(spmx_csr_upload(c.h, a.m, a.n, a.nnz, a.row_ptr.data(), a.col_indices.data(),
                           a.vals.data(), &h));
   }
-  // structure only (partition functions never read columns or values)
+  // structure only (partition functions never read columns or values): row_ptr is all that
+  // crosses the bus
   DevCsr(Ctx& c, int64_t m, int64_t nnz, const uint64_t* row_ptr) {
-    std::vector<uint32_t> col(size_t(nnz), 0u);
-    std::vector<float> vals(size_t(nnz), 0.0f);
-    check(spmx_csr_upload(c.h, m, 1, nnz, row_ptr, col.data(), vals.data(), &h));
+    check(spmx_rowptr_upload(c.h, m, nnz, row_ptr, &h));
   }
   ~DevCsr() { if (h) spmx_csr_destroy(h); }
   DevCsr(const DevCsr&) = delete;
@@ -123,12 +123,23 @@ inline std::vector<RowRange> to_ranges(const std::vector<uint64_t>& flat) {
 
 inline double now_s();
 
+// One context per host thread and device, created on first use and kept for the thread's
+// lifetime: the reference's entry points hold no global state and may be called concurrently
+// (SPEC.md:342), a context belongs to one host thread at a time (include/spmx_b200.h).
+inline Ctx& thread_ctx(int device = 0) {
+  thread_local std::vector<std::unique_ptr<Ctx>> per_device;
+  if (device < 0) throw std::invalid_argument("no such device");
+  if (per_device.size() <= size_t(device)) per_device.resize(size_t(device) + 1);
+  if (!per_device[size_t(device)]) per_device[size_t(device)] = std::make_unique<Ctx>(device);
+  return *per_device[size_t(device)];
+}
+
 }  // namespace detail
 
 // ---- partitioner (partition.hpp:44-68), computed on the device, bit-exact ----------------------
 inline std::vector<RowRange> split_rows_static(uint64_t m, unsigned threads) {
   if (threads == 0) throw std::invalid_argument("split_rows_static: zero threads");
-  detail::Ctx c;
+  detail::Ctx& c = detail::thread_ctx();
   std::vector<uint64_t> flat(2 * size_t(threads));
   detail::check(spmx_split_rows_static(c.h, m, threads, flat.data()));
   return detail::to_ranges(flat);
@@ -136,7 +147,7 @@ inline std::vector<RowRange> split_rows_static(uint64_t m, unsigned threads) {
 
 inline std::vector<RowRange> split_nnz(const CsrMatrix& a, unsigned threads) {
   if (threads == 0) throw std::invalid_argument("split_nnz: zero threads");
-  detail::Ctx c;
+  detail::Ctx& c = detail::thread_ctx();
   detail::DevCsr d(c, a.m, a.nnz, a.row_ptr.data());
   std::vector<uint64_t> flat(2 * size_t(threads));
   detail::check(spmx_split_nnz(c.h, d.h, threads, flat.data()));
@@ -145,7 +156,7 @@ inline std::vector<RowRange> split_nnz(const CsrMatrix& a, unsigned threads) {
 
 inline std::vector<RowRange> split_merge(const CsrMatrix& a, unsigned threads) {
   if (threads == 0) throw std::invalid_argument("split_merge: zero threads");
-  detail::Ctx c;
+  detail::Ctx& c = detail::thread_ctx();
   detail::DevCsr d(c, a.m, a.nnz, a.row_ptr.data());
   std::vector<uint64_t> flat(2 * size_t(threads));
   detail::check(spmx_split_merge(c.h, d.h, threads, flat.data()));
@@ -157,7 +168,7 @@ inline std::vector<RowRange> split_merge(const CsrMatrix& a, unsigned threads) {
 inline MergeCoordinate merge_path_search(uint64_t k, const uint64_t* row_end, uint64_t m,
                                          uint64_t nnz) {
   if (k > m + nnz) throw std::invalid_argument("merge_path_search: diagonal out of range");
-  detail::Ctx c;
+  detail::Ctx& c = detail::thread_ctx();
   detail::DevCsr d(c, int64_t(m), int64_t(nnz), row_end - 1);
   MergeCoordinate out;
   detail::check(spmx_merge_path_search(c.h, d.h, 1, &k, &out.i, &out.j));
@@ -167,7 +178,7 @@ inline MergeCoordinate merge_path_search(uint64_t k, const uint64_t* row_end, ui
 // many diagonals at once (one upload): the efficient form of the call above
 inline std::vector<MergeCoordinate> merge_path_search(const CsrMatrix& a,
                                                       const std::vector<uint64_t>& ks) {
-  detail::Ctx c;
+  detail::Ctx& c = detail::thread_ctx();
   detail::DevCsr d(c, a.m, a.nnz, a.row_ptr.data());
   std::vector<uint64_t> oi(ks.size()), oj(ks.size());
   detail::check(spmx_merge_path_search(c.h, d.h, ks.size(), ks.data(), oi.data(), oj.data()));
@@ -235,7 +246,7 @@ inline constexpr double kVerifyTolerance = 1e-5;
 inline double max_relative_error(const DenseMatrix& y, const DenseMatrix& ref) {
   if (y.data.size() != ref.data.size())
     throw std::invalid_argument("max_relative_error: shape mismatch");
-  detail::Ctx c;
+  detail::Ctx& c = detail::thread_ctx();
   const size_t bytes = y.data.size() * sizeof(float);
   detail::DevBuf dy(c, bytes), dr(c, bytes);
   detail::check(spmx_h2d(c.h, dy.p, y.data.data(), bytes));
@@ -263,7 +274,7 @@ inline uint64_t checksum(const DenseMatrix& y) {
 // reference.hpp:11 — Alg. 1 (unfused), evaluated on the device
 inline DenseMatrix spmm_reference(const CsrMatrix& a, const DenseMatrix& x) {
   if (a.n != x.rows) throw std::invalid_argument("spmm_reference: A.n != X.rows");
-  detail::Ctx c;
+  detail::Ctx& c = detail::thread_ctx();
   detail::DevCsr da(c, a);
   DenseMatrix y(a.m, x.cols);
   detail::DevBuf dx(c, x.data.size() * 4), dy(c, y.data.size() * 4);
@@ -288,7 +299,7 @@ inline std::pair<DenseMatrix, RunReport> run_spmm(const CsrMatrix& a, const Dens
   const unsigned flags = (cfg.backend == Backend::Interp ? SPMX_EXACT_ORDER : 0u) |
                          (jit ? SPMX_JIT_WIDTH : 0u);
 
-  detail::Ctx c(cfg.device);
+  detail::Ctx& c = detail::thread_ctx(cfg.device);
   detail::DevCsr da(c, a);
   const int64_t d = x.cols;
   DenseMatrix y(a.m, d);

@@ -264,6 +264,46 @@ def plan_patch(code, log=None):
             if not any(0 < dist(k, w) <= dist(k, cons[k]) for w in waits):
                 say("a moved gather would not be waited for")
                 return None
+    # Control flow. The dependence model above is linear (address order inside the loop body),
+    # which is only sound when the body is a single-entry straight trunk with forward skips:
+    #   * nothing outside the loop jumps into the body, and the body holds no indirect
+    #     branch, call or return;
+    #   * every branch inside the body is a forward branch that stays inside the body (a
+    #     conditionally skipped region, e.g. the row-end block) or the back edge itself;
+    #   * every instruction that receives a new wait lies on the trunk: no forward branch
+    #     jumps over it, so EVERY path from a moved gather to any of its consumers executes
+    #     the wait (a wait inside a skipped region would leave the real consumer unguarded);
+    #   * a moved gather may itself be skipped (then it never signals the scoreboard and the
+    #     wait passes), but no consumer of its registers may precede the wait in address order
+    #     after it, which the cyclic check above established.
+    lo_addr, hi_addr = body[0].addr, body[-1].addr
+    for c in code:
+        mb = re.search(_BRA, c.text)
+        if mb and not (lo_addr <= c.addr <= hi_addr) and lo_addr < int(mb.group(1), 16) <= hi_addr:
+            say("a branch from outside enters the loop body")
+            return None
+    skips = []  # (index of the branch, index of its target) for forward branches in the body
+    for k, c in enumerate(body):
+        if re.search(r"\b(BRX|JMP|JMX|CALL|RET|EXIT|BREAK|BRXU|JMXU)\b", c.text):
+            say(f"unsupported control flow in the loop body: {c.text}")
+            return None
+        mb = re.search(_BRA, c.text)
+        if not mb or k == n - 1:
+            continue
+        tgt = int(mb.group(1), 16)
+        if not (c.addr < tgt <= hi_addr):
+            say(f"a branch leaves the loop body or goes backwards: {c.text}")
+            return None
+        ti = next((j for j, cc in enumerate(body) if cc.addr == tgt), None)
+        if ti is None:
+            say("branch target not on an instruction boundary")
+            return None
+        skips.append((k, ti))
+    for w in waits:
+        if any(b < w < t for b, t in skips):
+            say(f"the wait at {body[w].addr:#x} can be jumped over: not on the loop's trunk")
+            return None
+    # (store-barrier pairs moved by _free_store_barrier were matched inside straight-line runs)
     edits = [(top + k, hi) for k, hi in sorted(his.items())]
     half = [k for t in moved_events for k in events[t]]
     wait_at = waits[0]
@@ -272,29 +312,55 @@ def plan_patch(code, log=None):
     return edits
 
 
+MARKER = b"SPMX_SASS_SCHED=0;"  # csrc/spmx_capi.cu: spmx_build_info(); rewritten after a patch
+
+
+class SassSchedError(RuntimeError):
+    """A precompiled width could not be re-scheduled (the preconditions no longer hold)."""
+
+
 def patch_library(lib, kernels=("spmm_chunk_kernelILi64ELi8ELi4ELi2ELb0", "spmm_dynamic_kernelILi64ELi8ELi4ELi2ELb0",
                                 "spmm_chunk_kernelILi32ELi8ELi4ELi1ELb0", "spmm_dynamic_kernelILi32ELi8ELi4ELi1ELb0",
                                 "spmm_chunk_kernelILi128ELi8ELi4ELi4ELb0", "spmm_dynamic_kernelILi128ELi8ELi4ELi4ELb0"),
-                  dry_run=False, log=print):
+                  dry_run=False, log=print, strict=False):
+    """Re-schedules the listed kernels inside `lib`. With strict=True (the build) a listed
+    kernel that is missing or fails a precondition raises SassSchedError instead of being
+    left as compiled, so that a toolchain change cannot silently ship the slower schedule.
+    The library's build-info string records how many kernels were edited."""
     funcs = disassemble(lib)
     data = bytearray(open(lib, "rb").read())
-    done = 0
+    done, failed = 0, []
+    seen = set()
     for name, code in funcs.items():
-        if not any(k in name for k in kernels) or not code:
+        hit = next((k for k in kernels if k in name), None)
+        if hit is None or not code:
             continue
+        seen.add(hit)
         blob = b"".join(c.bytes() for c in code)
         pos = data.find(blob)
         if pos < 0 or data.find(blob, pos + 1) >= 0:
             log(f"{name[:60]}: code not located uniquely (already patched or compressed)")
+            failed.append(hit)
             continue
         edits = plan_patch(code, lambda s: log(f"{name[:60]}: {s}"))
         if not edits:
+            failed.append(hit)
             continue
         for idx, hi in edits:
             o = pos + 16 * idx + 8
             data[o:o + 8] = hi.to_bytes(8, "little")
         done += 1
+    failed += [k for k in kernels if k not in seen]
+    if strict and failed:
+        raise SassSchedError("sass_sched: preconditions failed for " + ", ".join(failed) +
+                             " (set SPMX_NO_SASS_SCHED=1 to ship the schedule as compiled)")
     if done and not dry_run:
+        pos = data.find(MARKER)
+        if pos >= 0 and data.find(MARKER, pos + 1) < 0:
+            new = MARKER.replace(b"=0;", b"=%d;" % min(done, 9))
+            data[pos:pos + len(MARKER)] = new
+        elif strict:
+            raise SassSchedError("sass_sched: build-info marker not found in the library")
         open(lib, "wb").write(bytes(data))
     return done
 

@@ -29,7 +29,7 @@ def test_library_exports_every_declared_symbol():
     lib = ctypes.CDLL(binding.LIB_PATH)
     missing = [s for s in declared_symbols() if not hasattr(lib, s)]
     assert not missing, missing
-    assert lib.spmx_abi_version() == 1
+    assert lib.spmx_abi_version() == 2
 
 
 def test_no_cpu_fallback():

@@ -52,3 +52,95 @@ def test_extreme_rows(ctx, oracle, lens, n, d):
         if nnz > 100_000:
             cr, cj = p.chunks()
             assert chain_lengths(m, cr, cj, rp).max() > 1000  # the long-chain path did the work
+
+
+def _poison_carry_pool(ctx, rng):
+    """Fills the stream-ordered pool with non-zero garbage where a later plan's carry rows
+    will live: run a merge plan whose rows are all cut (large partial sums), then free it."""
+    m, n, d = 3, 2000, 64
+    lens = np.array([300_000, 200_000, 250_000], np.uint64)
+    rp = np.zeros(m + 1, np.uint64)
+    rp[1:] = np.cumsum(lens)
+    nnz = int(rp[-1])
+    col = rng.integers(0, n, size=nnz, dtype=np.int64).astype(np.uint32)
+    vals = np.full(nnz, 1000.0, np.float32)
+    x = np.full((n, d), 7.0, np.float32)
+    a = ctx.csr_upload(m, n, rp, col, vals)
+    p = ctx.plan(a, "merge", 0)
+    yd = torch.empty(m, d, device="cuda")
+    ctx.spmm(p, a, torch.from_numpy(x).cuda(), yd)
+    ctx.synchronize()
+    p.close()
+    a.close()
+
+
+@pytest.mark.parametrize("m,row_nnz,parts", [(1, 1, 4), (1, 1, 64), (2, 3, 50), (5, 2, 301), (3, 40, 1000)])
+def test_more_parts_than_merge_items(ctx, oracle, m, row_nnz, parts):
+    """merge-split with parts >> m + nnz: duplicate diagonals give empty chunks that sit inside
+    a row's carry chain. Their partial is zero by definition; the carry buffer comes from the
+    stream-ordered pool unzeroed, so the empty chunk itself must write that zero. Run after
+    the pool has been filled with large values, twice, on several widths."""
+    rng = np.random.default_rng(11)
+    n = 37
+    rp = np.arange(m + 1, dtype=np.uint64) * np.uint64(row_nnz)
+    nnz = int(rp[-1])
+    col = rng.integers(0, n, size=nnz, dtype=np.int64).astype(np.uint32)
+    vals = (rng.random(nnz, np.float32) + 0.5).astype(np.float32)
+    for d in (64, 32, 5, 128):
+        x = (rng.random((n, d), np.float32) + 0.5).astype(np.float32)
+        unf = oracle.spmm_unfused(m, n, rp, col, vals, x)
+        bound = oracle.abs_bound(m, rp, col, vals, x)
+        for rep in range(2):
+            _poison_carry_pool(ctx, rng)
+            a = ctx.csr_upload(m, n, rp, col, vals)
+            p = ctx.plan(a, "merge", parts)
+            yd = torch.full((m, d), float("nan"), device="cuda")
+            ctx.spmm(p, a, torch.from_numpy(x).cuda(), yd)
+            ctx.synchronize()
+            assert north_star_ok(yd.cpu().numpy(), unf, bound), (d, rep, yd.cpu().numpy()[:, :4], unf[:, :4])
+            p.close()
+            a.close()
+
+
+def test_invalid_column_under_dynamic_dispatch_is_einval(ctx):
+    """spmx_spmm_host validates column indices on the device while the kernels are queued: an
+    out-of-range column must come back as SPMX_EINVAL for dynamic row dispatch too (the
+    reference's default mode), not as an illegal-address fault."""
+    from paper_2312_05639_b200.binding import SpmxInvalidArgument
+    rng = np.random.default_rng(3)
+    m, n, d = 4000, 300, 64
+    lens = rng.integers(0, 40, size=m)
+    rp = np.zeros(m + 1, np.uint64)
+    rp[1:] = np.cumsum(lens.astype(np.uint64))
+    nnz = int(rp[-1])
+    col = rng.integers(0, n, size=nnz, dtype=np.int64).astype(np.uint32)
+    col[nnz // 2] = np.uint32(0x7fffff00)  # far outside X
+    vals = rng.random(nnz, np.float32)
+    x = rng.random((n, d), np.float32)
+    for dyn in (True, False):
+        with pytest.raises(SpmxInvalidArgument, match="column index out of range"):
+            ctx.spmm_host(m, n, rp, col, vals, x, strategy="row", dynamic=dyn)
+    # the context is still usable afterwards (no sticky CUDA error)
+    col[nnz // 2] = 0
+    y, _ = ctx.spmm_host(m, n, rp, col, vals, x, strategy="row", dynamic=True)
+    assert np.isfinite(y).all()
+
+
+def test_structure_only_handle(ctx, oracle):
+    """spmx_rowptr_upload: partitioner and plans work from row_ptr alone; SpMM refuses it."""
+    from paper_2312_05639_b200.binding import SpmxLogicError
+    rng = np.random.default_rng(1)
+    m = 5000
+    lens = rng.integers(0, 30, size=m)
+    rp = np.zeros(m + 1, np.uint64)
+    rp[1:] = np.cumsum(lens.astype(np.uint64))
+    s = ctx.rowptr_upload(m, rp)
+    for parts in (1, 7, 64):
+        assert np.array_equal(ctx.split_nnz(s, parts), oracle.split_nnz(rp, parts))
+        assert np.array_equal(ctx.split_merge(s, parts), oracle.split_merge(rp, parts))
+    p = ctx.plan(s, "merge", 16)
+    assert np.array_equal(p.ranges(), oracle.split_merge(rp, 16))
+    with pytest.raises(SpmxLogicError):
+        ctx.spmm(p, s, torch.zeros(1, 4, device="cuda"), torch.zeros(m, 4, device="cuda"))
+    p.close()
+    s.close()

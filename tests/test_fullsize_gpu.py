@@ -1,11 +1,28 @@
-"""Parity at BASELINE.json's full sizes (c2, c3, c4), through properties that do not need a
-whole-matrix CPU pass: (1) exact-order results are bitwise identical across the three
-strategies and part counts (the reference's own invariant, test_executor.cpp:67-87),
-(2) a sample of rows — the heaviest, empty ones, random ones — equals the oracle bitwise in
-exact-order mode and obeys the north_star bound in default mode, (3) default mode stays
-within the bound of exact-order mode everywhere (device-side check), (4) linearity,
-(5) a permutation matrix returns the permuted X bitwise. c5 (8.6 GB operands) is covered by
-the same kernels at d = 128 through c3; bench.py --workload c5 runs it."""
+"""Parity at BASELINE.json's FULL sizes: every division scheme on c2, c3, c4 and c5.
+
+north_star: "Y matches the CPU oracle within tolerance for all three division schemes on all
+five configs" (c1 is whole-matrix in test_spmm_gpu.py). For each config the UNMODIFIED reference
+(oracle/_ref/libspmx_ref.so: run_spmm, Backend::Native, all host threads,
+/root/reference/proj/src/executor.cpp:36-112) computes the whole matrix once on the box's CPU;
+then, for each of row / nnz / merge:
+
+  * SPMX_EXACT_ORDER: the device result is BITWISE equal to the reference's over the whole
+    matrix (the reference's own invariant: one result for every strategy and thread count,
+    tests/test_executor.cpp:67-87, native == interpreter tests/test_jit.cpp:92-113);
+  * default mode: |y - y_ref| <= 1e-5 * sum_j |a_ij * x_j| + 1e-6 for EVERY element against the
+    reference's result (tests/acceptance.cpp:69-124 states the same bar with max_relative_error),
+    the magnitude sum evaluated in float64 by plain torch ops (not by the kernel under test) and
+    itself cross-checked against the C oracle on the sampled rows; rows that no chunk boundary
+    cuts are bitwise equal to the reference.
+
+A sample of rows (the heaviest, empty ones, first/last, random ones) is also compared with the C
+restatement (oracle/spmx_oracle.c): fused bitwise, unfused spmm_reference semantics
+(src/reference.cpp:10-25) within the bound. c5 is the one config with M*d = 2^31 elements
+(64-bit offsets, > 2^31-byte X and Y). If oracle/_ref was not built the whole-matrix legs are
+skipped and the sampled rows + cross-strategy invariance remain.
+"""
+import os
+
 import numpy as np
 import pytest
 import torch
@@ -13,100 +30,194 @@ import torch
 pytestmark = pytest.mark.gpu
 
 EXACT = 1
-CASES = [("c2", ("row", "nnz", "merge")), ("c4", ("merge", "row")), ("c3", ("nnz",))]
+CONFIGS = ["c2", "c3", "c4", "c5"]
+STRATEGIES = ["row", "nnz", "merge"]
+TOL_REL, TOL_ABS = 1e-5, 1e-6  # BASELINE.json north_star
+
+
+def _host_threads():
+    return len(os.sched_getaffinity(0)) if hasattr(os, "sched_getaffinity") else (os.cpu_count() or 1)
+
+
+def abs_bound_torch(a, x, block_nnz=1 << 21):
+    """sum_j |a_ij| * |x_jk| in float64 for every (i, k): plain torch gathers and index_add over
+    row blocks of about block_nnz nonzeros. Independent of the library under test."""
+    d = x.shape[1]
+    out = torch.zeros(a.m, d, dtype=torch.float64, device=x.device)
+    rp = a.row_ptr
+    lens = rp[1:] - rp[:-1]
+    r = 0
+    while r < a.m:
+        lo = int(rp[r])
+        r1 = int(torch.searchsorted(rp, torch.tensor(lo + block_nnz, device=rp.device), right=True)) - 1
+        r1 = min(max(r1, r + 1), a.m)
+        hi = int(rp[r1])
+        if hi > lo:
+            cols = a.col[lo:hi].long() & 0xFFFFFFFF
+            prod = a.vals[lo:hi].abs().double().unsqueeze(1) * x[cols].abs().double()
+            rows_local = torch.repeat_interleave(torch.arange(r1 - r, device=x.device), lens[r:r1])
+            out[r:r1].index_add_(0, rows_local, prod)
+            del cols, prod, rows_local
+        r = r1
+    return out
 
 
 def _sample_rows(a, rng, k=300):
-    lens = (a.row_ptr[1:] - a.row_ptr[:-1])
+    lens = a.row_ptr[1:] - a.row_ptr[:-1]
     heavy = torch.topk(lens, 12).indices.cpu().numpy()
     empty = torch.nonzero(lens == 0)[:40, 0].cpu().numpy()
     rnd = rng.integers(0, a.m, size=k)
     return np.unique(np.concatenate([heavy, empty, rnd, [0, a.m - 1]]))
 
 
-def _oracle_rows(oracle, a, x_host, rows):
-    """Fused and unfused oracle results plus the magnitude bound for the given rows only."""
+def _oracle_rows(oracle, a, x, rows):
+    """Fused and unfused C-oracle results plus the float64 magnitude bound for `rows` only. The
+    X rows those rows touch are gathered into a compact matrix first (c5's X is 8.6 GB)."""
     rp = a.row_ptr.cpu().numpy().astype(np.int64)
-    col_t, val_t = a.col, a.vals
-    d = x_host.shape[1]
+    d = x.shape[1]
     fused = np.zeros((len(rows), d), np.float32)
     unf = np.zeros((len(rows), d), np.float32)
     bound = np.zeros((len(rows), d), np.float64)
     for i, r in enumerate(rows):
-        lo, hi = rp[r], rp[r + 1]
-        c = col_t[lo:hi].cpu().numpy().view(np.uint32)
-        v = val_t[lo:hi].cpu().numpy()
+        lo, hi = int(rp[r]), int(rp[r + 1])
+        c = a.col[lo:hi].long() & 0xFFFFFFFF
+        uniq, inv = torch.unique(c, return_inverse=True)
+        xs = x[uniq].cpu().numpy() if hi > lo else np.zeros((1, d), np.float32)
+        cl = inv.cpu().numpy().astype(np.uint32)
+        v = a.vals[lo:hi].cpu().numpy()
         rp1 = np.array([0, hi - lo], np.uint64)
-        fused[i] = oracle.spmm_fused(1, a.n, rp1, c, v, x_host, threads=1)[0]
-        unf[i] = oracle.spmm_unfused(1, a.n, rp1, c, v, x_host)[0]
-        bound[i] = oracle.abs_bound(1, rp1, c, v, x_host)[0]
+        n_small = xs.shape[0]
+        fused[i] = oracle.spmm_fused(1, n_small, rp1, cl, v, xs, threads=1)[0]
+        unf[i] = oracle.spmm_unfused(1, n_small, rp1, cl, v, xs)[0]
+        bound[i] = oracle.abs_bound(1, rp1, cl, v, xs)[0]
     return fused, unf, bound
 
 
-@pytest.mark.parametrize("name,strategies", CASES)
-def test_full_size_config(ctx, oracle, name, strategies):
+class Case:
+    pass
+
+
+@pytest.fixture(scope="module", params=CONFIGS)
+def case(request, ctx, oracle):
+    """One full-size config: inputs on the device, the reference's whole-matrix result, the
+    float64 magnitude bound and the sampled-row oracle results. Built once per config."""
+    from oracle.pyoracle import RefLib
     from paper_2312_05639_b200 import workloads as W
-    a, x, spec = W.make_config(name, device="cuda")
+    name = request.param
+    c = Case()
+    c.name = name
+    c.a, c.x, c.spec = W.make_config(name, device="cuda")
     torch.cuda.synchronize()
-    d = spec["d"]
-    da = ctx.csr_wrap(a)
+    c.d = c.spec["d"]
+    c.da = ctx.csr_wrap(c.a)
     rng = np.random.default_rng(7)
-    rows = _sample_rows(a, rng)
-    x_host = x.cpu().numpy()
-    fused, unf, bound = _oracle_rows(oracle, a, x_host, rows)
-    rows_t = torch.from_numpy(rows).cuda()
+    c.rows = _sample_rows(c.a, rng)
+    c.rows_t = torch.from_numpy(c.rows).cuda()
+    c.fused, c.unf, c.row_bound = _oracle_rows(oracle, c.a, c.x, c.rows)
+    c.bound = abs_bound_torch(c.a, c.x)
+    # the torch bound agrees with the C oracle's on the sampled rows (float64, order differs)
+    got_b = c.bound[c.rows_t].cpu().numpy()
+    assert np.allclose(got_b, c.row_bound, rtol=1e-12, atol=0.0), name
+    c.y_ref = None       # the reference's whole-matrix result, on the device
+    c.y_exact = None     # first exact-order device result (cross-strategy invariance)
+    if RefLib.available():
+        ref = RefLib()
+        rp, col, vals = c.a.numpy()
+        ra = ref.csr(c.a.m, c.a.n, rp, col, vals)
+        del rp, col, vals
+        xh = c.x.cpu().numpy()
+        y_cpu, rep = ref.run_spmm(ra, xh, "nnz", False, _host_threads(), "native", 128, 1)
+        del xh, ra
+        c.ref_threads = rep["threads"]
+        c.y_ref = torch.from_numpy(y_cpu).cuda()
+        del y_cpu
+        # the reference's fused result equals the C restatement on the sampled rows, bitwise
+        assert np.array_equal(c.y_ref[c.rows_t].cpu().numpy().view(np.uint32), c.fused.view(np.uint32)), name
+    torch.cuda.synchronize()
+    yield c
+    c.da.close()
+    del c.a, c.x, c.bound, c.y_ref, c.y_exact
+    torch.cuda.empty_cache()
 
-    y_ref = None
-    for s in strategies:
-        for parts in (0, 1000):
-            p = ctx.plan(da, s, parts, flags=EXACT)
-            y = torch.full((a.m, d), float("nan"), device="cuda")
-            ctx.spmm(p, da, x, y)
-            ctx.synchronize()
-            got = y[rows_t].cpu().numpy()
-            assert np.array_equal(got.view(np.uint32), fused.view(np.uint32)), (name, s, parts)
-            if y_ref is None:
-                y_ref = y
-            else:  # bitwise identical across strategies and part counts
-                assert torch.equal(y.view(torch.int32), y_ref.view(torch.int32)), (name, s, parts)
-            p.close()
-    assert not torch.isnan(y_ref).any()
 
-    # default mode: sampled rows within the north_star bound of the unfused reference; whole
-    # result within the bound of the exact-order result (bound evaluated on the device)
-    absx = x.abs()
-    absa = W.Csr(a.m, a.n, a.nnz, a.row_ptr, a.col, a.vals.abs())
-    torch.cuda.synchronize()  # the context runs on its own stream: inputs must be complete
-    dabs = ctx.csr_wrap(absa, validate=False)
-    pb = ctx.plan(dabs, "merge", 0, flags=EXACT)
-    s_bound = torch.empty(a.m, d, device="cuda")
-    ctx.spmm(pb, dabs, absx, s_bound)   # sum |a*x| in fp32 (an upper-bound proxy, > 0.99 of fp64)
-    ctx.synchronize()
-    for s in strategies:
-        p = ctx.plan(da, s, 0)
-        y = torch.full((a.m, d), float("nan"), device="cuda")
-        ctx.spmm(p, da, x, y)
+def _bitwise_equal(y, ref, block=1 << 20):
+    for r in range(0, y.shape[0], block):
+        if not torch.equal(y[r:r + block].view(torch.int32), ref[r:r + block].view(torch.int32)):
+            return False
+    return True
+
+
+def _within_bound(y, ref, bound, block=1 << 19):
+    for r in range(0, y.shape[0], block):
+        err = (y[r:r + block].double() - ref[r:r + block].double()).abs()
+        if not bool((err <= TOL_REL * bound[r:r + block] + TOL_ABS).all()):
+            return False
+    return True
+
+
+@pytest.mark.parametrize("strategy", STRATEGIES)
+def test_exact_order_is_bitwise_the_reference(ctx, case, strategy):
+    c = case
+    for parts in (0, 1000):
+        p = ctx.plan(c.da, strategy, parts, flags=EXACT)
+        y = torch.full((c.a.m, c.d), float("nan"), device="cuda")
+        ctx.spmm(p, c.da, c.x, y)
         ctx.synchronize()
-        got = y[rows_t].cpu().numpy()
-        assert np.all(np.abs(got.astype(np.float64) - unf) <= 1e-5 * bound + 1e-6), (name, s)
-        err = (y.double() - y_ref.double()).abs()
-        assert bool((err <= 1e-5 * s_bound.double() * 1.01 + 1e-6).all()), (name, s)
-        # rows not cut by any chunk boundary are bitwise equal to exact-order mode
-        cr, cj = p.chunks()
-        cut = np.zeros(a.m, bool)
-        rp = a.row_ptr.cpu().numpy()
-        inner_r, inner_j = cr[1:-1].astype(np.int64), cj[1:-1].astype(np.int64)
-        ok = inner_r < a.m
-        is_cut = np.zeros_like(ok)
-        is_cut[ok] = inner_j[ok] > rp[inner_r[ok]]
-        cut[inner_r[is_cut]] = True
-        keep = torch.from_numpy(~cut).cuda()
-        assert torch.equal(y[keep].view(torch.int32), y_ref[keep].view(torch.int32)), (name, s)
-        assert cut.sum() < 0.05 * a.m
         p.close()
-    pb.close()
-    dabs.close()
-    da.close()
+        # sampled rows against the C restatement
+        got = y[c.rows_t].cpu().numpy()
+        assert np.array_equal(got.view(np.uint32), c.fused.view(np.uint32)), (c.name, strategy, parts)
+        # whole matrix against the unmodified reference's run_spmm
+        if c.y_ref is not None:
+            assert _bitwise_equal(y, c.y_ref), (c.name, strategy, parts, "differs from the reference")
+        # and the reference's own invariant: one result for every strategy and part count
+        if c.y_exact is None:
+            assert not torch.isnan(y).any()
+            c.y_exact = y
+        else:
+            assert _bitwise_equal(y, c.y_exact), (c.name, strategy, parts)
+    if c.y_ref is None:
+        pytest.skip("oracle/_ref/libspmx_ref.so not built: whole-matrix compare skipped "
+                    "(sampled rows and cross-strategy invariance checked)")
+
+
+@pytest.mark.parametrize("strategy", STRATEGIES)
+def test_default_mode_within_north_star_tolerance(ctx, case, strategy):
+    c = case
+    ref = c.y_ref if c.y_ref is not None else c.y_exact
+    if ref is None:  # this test selected alone, without the reference: make the exact result
+        p = ctx.plan(c.da, "nnz", 0, flags=EXACT)
+        ref = torch.empty(c.a.m, c.d, device="cuda")
+        ctx.spmm(p, c.da, c.x, ref)
+        ctx.synchronize()
+        p.close()
+        c.y_exact = ref
+    p = ctx.plan(c.da, strategy, 0)
+    y = torch.full((c.a.m, c.d), float("nan"), device="cuda")
+    ctx.spmm(p, c.da, c.x, y)
+    ctx.synchronize()
+    # sampled rows: within the bound of the UNFUSED reference semantics (src/reference.cpp:10-25)
+    got = y[c.rows_t].cpu().numpy()
+    assert np.all(np.abs(got.astype(np.float64) - c.unf) <= TOL_REL * c.row_bound + TOL_ABS), (c.name, strategy)
+    # every element: within the bound of the reference's CPU result
+    assert _within_bound(y, ref, c.bound), (c.name, strategy)
+    # rows not cut by any chunk boundary are bitwise the reference's
+    cr, cj = p.chunks()
+    p.close()
+    rp = c.a.row_ptr.cpu().numpy()
+    inner_r, inner_j = cr[1:-1].astype(np.int64), cj[1:-1].astype(np.int64)
+    ok = inner_r < c.a.m
+    is_cut = np.zeros_like(ok)
+    is_cut[ok] = inner_j[ok] > rp[inner_r[ok]]
+    cut = np.zeros(c.a.m, bool)
+    cut[inner_r[is_cut]] = True
+    assert cut.sum() < 0.05 * c.a.m
+    keep = torch.from_numpy(~cut).cuda()
+    block = 1 << 20
+    for r in range(0, c.a.m, block):
+        k = keep[r:r + block]
+        assert torch.equal(y[r:r + block][k].view(torch.int32), ref[r:r + block][k].view(torch.int32)), \
+            (c.name, strategy, "an uncut row differs")
 
 
 def test_linearity_and_permutation_full_size(ctx):
@@ -120,7 +231,6 @@ def test_linearity_and_permutation_full_size(ctx):
     da = ctx.csr_wrap(a)
     p = ctx.plan(da, "merge", 0)
     ys = []
-    torch.cuda.synchronize()  # the context runs on its own stream: inputs must be complete
     for xx in (x1, x2, 2 * x1 + x2):
         y = torch.empty(a.m, d, device="cuda")
         xx = xx.contiguous()
@@ -128,16 +238,9 @@ def test_linearity_and_permutation_full_size(ctx):
         ctx.spmm(p, da, xx, y)
         ctx.synchronize()
         ys.append(y)
-    absa = W.Csr(a.m, a.n, a.nnz, a.row_ptr, a.col, a.vals.abs())
-    dabs = ctx.csr_wrap(absa, validate=False)
-    pb = ctx.plan(dabs, "merge", 0)
-    sb = torch.empty(a.m, d, device="cuda")
-    xabs = (2 * x1.abs() + x2.abs()).contiguous()
-    torch.cuda.synchronize()
-    ctx.spmm(pb, dabs, xabs, sb)
-    ctx.synchronize()
+    sb = abs_bound_torch(a, (2 * x1.abs() + x2.abs()).contiguous())
     err = (ys[2].double() - (2 * ys[0].double() + ys[1].double())).abs()
-    assert bool((err <= 4e-5 * sb.double() + 4e-6).all())
+    assert bool((err <= 4e-5 * sb + 4e-6).all())
 
     m = 1 << 22
     perm = torch.randperm(m, device="cuda", generator=torch.Generator(device="cuda").manual_seed(5))

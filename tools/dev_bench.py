@@ -13,7 +13,7 @@ import torch
 
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 from paper_2312_05639_b200 import workloads as W  # noqa: E402
-from paper_2312_05639_b200.binding import Context, EXACT_ORDER, NO_COOP, JIT_WIDTH  # noqa: E402
+from paper_2312_05639_b200.binding import Context, EXACT_ORDER, JIT_WIDTH  # noqa: E402
 
 
 def main():
@@ -51,7 +51,7 @@ def main():
         ref = None
         for strat in args.strategies.split(","):
             for mode in args.modes.split(","):
-                flags = {"fast": 0, "exact": EXACT_ORDER, "nocoop": NO_COOP, "jit": JIT_WIDTH}[mode]
+                flags = {"fast": 0, "exact": EXACT_ORDER, "jit": JIT_WIDTH}[mode]
                 dyn = strat == "row-dyn"
                 tp = time.time()
                 p = ctx.plan(da, strat.split("-")[0], args.parts, dynamic=dyn, flags=flags)
