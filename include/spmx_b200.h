@@ -176,6 +176,12 @@ int spmx_jit_stats(uint64_t* kernels_compiled, double* seconds);
 /* 1 when the run-time compiler (libnvrtc) can be loaded, i.e. SPMX_JIT_WIDTH can be honoured */
 int spmx_jit_available(void);
 
+/* Measurement aid (bench.py roofline.gather): the L2 -> SM ceiling of this GPU at its current
+ * clocks — random 256-byte rows of an L2-resident 64 MB buffer read by 8-lane groups with
+ * LDG.128, 32 warps per SM (the SpMM's own access shape at d = 64); best of `repeats` launches,
+ * in TB/s over the whole chip, and that launch's duration. Not on the hot path. */
+int spmx_probe_l2_to_sm(spmx_ctx* ctx, int repeats, double* out_tbs, double* out_ms);
+
 /* ---- helpers for the reference's report fields ---------------------------------------------- */
 /* checksum(Y), dense.cpp:17-28, of a device buffer (FNV-1a is sequential: the buffer is copied
  * to the host and hashed there; a reporting helper, not on the hot path) */
@@ -255,18 +261,32 @@ int spmx_mg_broadcast_x_device(spmx_mg* mg, float* const* d_x_local, int root_ra
                                int64_t x_rows, int64_t d, float* bcast_ms);
 
 /* Y_g = A_g * X on every local shard (run_spmm's parallel region, executor.cpp:70-97, with
- * GPUs for threads). step_ms = max over this process's ranks of the device time of that rank's
- * shards (CUDA events on the rank's stream); ms_per_local_shard (may be NULL) gets each
- * shard's own time. The ranks never wait for each other. */
-int spmx_mg_spmm(spmx_mg* mg, float* step_ms, float* ms_per_local_shard);
+ * GPUs for threads), `steps` times back to back (the reference's trials loop, executor.cpp:68).
+ * step_ms = max over this process's ranks of the device time of that rank's launches (CUDA
+ * events on the rank's stream) / steps; ms_per_local_shard (may be NULL) gets each shard's own
+ * time in the last step. The ranks never wait for each other. The call returns when every
+ * local rank has finished. */
+int spmx_mg_spmm(spmx_mg* mg, int steps, float* step_ms, float* ms_per_local_shard);
 /* device pointer of local shard i's Y block ((row_end - row_begin) x d, owned by the driver) */
 int spmx_mg_y_shard(const spmx_mg* mg, int local_shard, float** d_y);
 /* the local shards' rows of Y into a host M x d matrix (other rows are left untouched) */
 int spmx_mg_download_y(spmx_mg* mg, float* y_host);
+/* every local shard's Y block into its own host buffer (host_per_local_shard[i]: rows_i x d
+ * floats): the per-process form of the call above (one process per GPU keeps only its rows) */
+int spmx_mg_download_y_shards(spmx_mg* mg, float* const* host_per_local_shard);
 /* optional: the full M x d Y on every GPU, one ncclBroadcast per shard in one group
  * (all-gather-v: shards have unequal row counts, nothing is padded) */
 int spmx_mg_allgather_y(spmx_mg* mg, float* elapsed_ms);
 int spmx_mg_y_full(const spmx_mg* mg, int local_rank, float** d_y_full);
+
+/* Statistics across ranks (max of the step time, sum of nonzeros ...): values[0..count) are
+ * reduced over all `world` ranks with one ncclAllReduce and written back; count <= 16. A process
+ * that drives several ranks passes its per-process figures (a sum counts them once). */
+#define SPMX_REDUCE_SUM 0
+#define SPMX_REDUCE_MAX 1
+int spmx_mg_allreduce(spmx_mg* mg, double* values, int count, int op);
+/* waits for every local rank's stream */
+int spmx_mg_synchronize(spmx_mg* mg);
 
 #ifdef __cplusplus
 }

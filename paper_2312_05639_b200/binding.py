@@ -150,6 +150,29 @@ class Lib:
         L.spmx_spmm_reference.argtypes = [vp, vp, vp, i64, i64, vp]
         L.spmx_max_relative_error.argtypes = [vp, vp, vp, sz, P(C.c_double)]
         L.spmx_jit_stats.argtypes = [P(u64), P(C.c_double)]
+        # multi-GPU driver
+        ip, fp = P(C.c_int), P(C.c_float)
+        L.spmx_mg_create.argtypes = [C.c_int, ip, C.c_int, P(vp)]
+        L.spmx_mg_unique_id.argtypes = [vp]
+        L.spmx_mg_create_rank.argtypes = [C.c_int, vp, C.c_int, C.c_int, C.c_int, vp, P(vp)]
+        L.spmx_mg_destroy.argtypes = [vp]
+        L.spmx_mg_info.argtypes = [vp, ip, ip, ip, ip, ip]
+        L.spmx_mg_shard_owner.argtypes = [C.c_int, C.c_int, C.c_int]
+        L.spmx_mg_shard_host.argtypes = [vp, i64, i64, i64, vp, vp, vp, C.c_int, vp]
+        L.spmx_mg_shard_device.argtypes = [vp, C.c_int, i64, i64, i64, vp, vp, vp, C.c_int, vp]
+        L.spmx_mg_shard_info.argtypes = [vp, C.c_int, ip, ip, P(u64), P(u64), P(u64)]
+        L.spmx_mg_plan.argtypes = [vp, C.c_int, C.c_uint, C.c_int, u64, C.c_uint]
+        L.spmx_mg_broadcast_x_host.argtypes = [vp, vp, C.c_int, i64, i64, fp, fp]
+        L.spmx_mg_broadcast_x_device.argtypes = [vp, P(vp), C.c_int, i64, i64, fp]
+        L.spmx_mg_spmm.argtypes = [vp, C.c_int, fp, fp]
+        L.spmx_mg_y_shard.argtypes = [vp, C.c_int, P(vp)]
+        L.spmx_mg_download_y.argtypes = [vp, vp]
+        L.spmx_mg_download_y_shards.argtypes = [vp, P(vp)]
+        L.spmx_probe_l2_to_sm.argtypes = [vp, C.c_int, P(C.c_double), P(C.c_double)]
+        L.spmx_mg_allgather_y.argtypes = [vp, fp]
+        L.spmx_mg_y_full.argtypes = [vp, C.c_int, P(vp)]
+        L.spmx_mg_allreduce.argtypes = [vp, P(C.c_double), C.c_int, C.c_int]
+        L.spmx_mg_synchronize.argtypes = [vp]
 
     def check(self, rc: int):
         if rc == 0:
@@ -345,6 +368,12 @@ class Context:
                                                         C.byref(out)))
         return out.value
 
+    def probe_l2_to_sm(self, repeats=10):
+        """(TB/s, ms): the L2 -> SM ceiling measured now, on this GPU (spmx_probe_l2_to_sm)."""
+        tbs, ms = C.c_double(), C.c_double()
+        self.L.check(self.L.lib.spmx_probe_l2_to_sm(self.h, repeats, C.byref(tbs), C.byref(ms)))
+        return tbs.value, ms.value
+
     def checksum(self, y) -> int:
         out = C.c_uint64()
         self.L.check(self.L.lib.spmx_checksum_device(self.h, _ptr(y), y.numel(), C.byref(out)))
@@ -399,3 +428,163 @@ class Plan:
                 self.close()
         except Exception:
             pass
+
+
+SHARD_BY = {"nnz": 1, "merge": 2}
+
+
+class MultiGpu:
+    """spmx_mg: the library's multi-GPU driver (row-block shards from split_nnz(A, G) /
+    split_merge(A, G), one NCCL broadcast of X, Y row-sharded, optional all-gather-v).
+
+    MultiGpu(devices=[0, 1, ...])              one process drives all GPUs (ncclCommInitAll)
+    MultiGpu.for_rank(device, rank, world, id) one process per GPU (torchrun); id from unique_id()
+    n_shards > world places several row blocks on a GPU (tests: one GPU stands in for a node)."""
+
+    def __init__(self, devices=(0,), n_shards=0, lib: "Lib | None" = None, _handle=None):
+        self.L = lib or Lib.get()
+        if _handle is not None:
+            self.h = _handle
+        else:
+            devs = (C.c_int * len(devices))(*devices)
+            h = C.c_void_p()
+            self.L.check(self.L.lib.spmx_mg_create(len(devices), devs, n_shards, C.byref(h)))
+            self.h = h
+        self._keep = []
+
+    @staticmethod
+    def unique_id(lib: "Lib | None" = None) -> bytes:
+        L = lib or Lib.get()
+        buf = C.create_string_buffer(128)
+        L.check(L.lib.spmx_mg_unique_id(buf))
+        return buf.raw
+
+    @classmethod
+    def for_rank(cls, device, rank, world, uid: "bytes | None", n_shards=0, stream=None,
+                 lib: "Lib | None" = None) -> "MultiGpu":
+        L = lib or Lib.get()
+        h = C.c_void_p()
+        idbuf = C.create_string_buffer(uid, 128) if uid is not None else None
+        L.check(L.lib.spmx_mg_create_rank(device, C.c_void_p(stream or 0), rank, world, n_shards,
+                                          idbuf, C.byref(h)))
+        return cls(lib=L, _handle=h)
+
+    def close(self):
+        if self.h:
+            self.L.check(self.L.lib.spmx_mg_destroy(self.h))
+            self.h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def info(self) -> dict:
+        v = [C.c_int() for _ in range(5)]
+        self.L.check(self.L.lib.spmx_mg_info(self.h, *[C.byref(x) for x in v]))
+        return dict(zip(("world", "local_ranks", "shards", "local_shards", "nccl_version"),
+                        (x.value for x in v)))
+
+    def shard_owner(self, shard) -> int:
+        i = self.info()
+        return self.L.lib.spmx_mg_shard_owner(i["shards"], i["world"], shard)
+
+    def shard_host(self, m, n, row_ptr, col, vals, by="nnz"):
+        rp = _np_u64(row_ptr)
+        nnz = int(rp[m])
+        col = np.ascontiguousarray(col, dtype=np.uint32)
+        vals = np.ascontiguousarray(vals, dtype=np.float32)
+        out = np.zeros(2 * self.info()["shards"], np.uint64)
+        self.L.check(self.L.lib.spmx_mg_shard_host(self.h, m, n, nnz, _ptr(rp), _ptr(col) if col.size else 0,
+                                                   _ptr(vals) if vals.size else 0, SHARD_BY[by], _ptr(out)))
+        return out.reshape(-1, 2)
+
+    def shard_device(self, csr, by="nnz", src_local_rank=0):
+        """csr: workloads.Csr whose tensors live on local rank src_local_rank's GPU."""
+        out = np.zeros(2 * self.info()["shards"], np.uint64)
+        self.L.check(self.L.lib.spmx_mg_shard_device(self.h, src_local_rank, csr.m, csr.n, csr.nnz,
+                                                     _ptr(csr.row_ptr), _ptr(csr.col), _ptr(csr.vals),
+                                                     SHARD_BY[by], _ptr(out)))
+        return out.reshape(-1, 2)
+
+    def shard_info(self, local_shard) -> dict:
+        g, dev = C.c_int(), C.c_int()
+        b, e, z = C.c_uint64(), C.c_uint64(), C.c_uint64()
+        self.L.check(self.L.lib.spmx_mg_shard_info(self.h, local_shard, C.byref(g), C.byref(dev),
+                                                   C.byref(b), C.byref(e), C.byref(z)))
+        return dict(shard=g.value, device=dev.value, row_begin=b.value, row_end=e.value, nnz=z.value)
+
+    def local_shards(self):
+        return [self.shard_info(i) for i in range(self.info()["local_shards"])]
+
+    def plan(self, strategy="merge", parts=0, dynamic=False, batch=128, flags=0):
+        s = STRATEGY[strategy] if isinstance(strategy, str) else strategy
+        self.L.check(self.L.lib.spmx_mg_plan(self.h, s, parts, int(dynamic), batch, flags))
+
+    def broadcast_x_host(self, x, root=0):
+        """x: numpy N x d on the process that drives `root` (None elsewhere). Returns (h2d_ms, bcast_ms)."""
+        h2d, bc = C.c_float(), C.c_float()
+        if x is not None:
+            x = np.ascontiguousarray(x, dtype=np.float32)
+            self._shape = x.shape
+        rows, d = self._shape
+        self.L.check(self.L.lib.spmx_mg_broadcast_x_host(self.h, _ptr(x) if x is not None else 0, root,
+                                                         rows, d, C.byref(h2d), C.byref(bc)))
+        return h2d.value, bc.value
+
+    def set_x_shape(self, rows, d):
+        self._shape = (rows, d)
+
+    def broadcast_x_device(self, xs, root=0):
+        """xs: one N x d float32 tensor per local rank, on that rank's GPU (the root's holds X)."""
+        rows, d = xs[0].shape
+        arr = (C.c_void_p * len(xs))(*[_ptr(x) for x in xs])
+        bc = C.c_float()
+        self.L.check(self.L.lib.spmx_mg_broadcast_x_device(self.h, arr, root, rows, d, C.byref(bc)))
+        self._keep = list(xs)
+        self._shape = (rows, d)
+        return bc.value
+
+    def spmm(self, steps=1, per_shard=False):
+        ms = C.c_float()
+        n = self.info()["local_shards"]
+        per = (C.c_float * max(n, 1))()
+        self.L.check(self.L.lib.spmx_mg_spmm(self.h, steps, C.byref(ms), per if per_shard else None))
+        return (ms.value, list(per)[:n]) if per_shard else ms.value
+
+    def download_y(self, y=None, m=None):
+        rows, d = self._shape
+        if y is None:
+            y = np.zeros((m, d), np.float32)
+        self.L.check(self.L.lib.spmx_mg_download_y(self.h, _ptr(y)))
+        return y
+
+    def download_y_shards(self, blocks):
+        """blocks: one host array / tensor (rows_i x d float32) per local shard."""
+        arr = (C.c_void_p * max(len(blocks), 1))(*[_ptr(b) for b in blocks])
+        self.L.check(self.L.lib.spmx_mg_download_y_shards(self.h, arr))
+
+    def y_shard_ptr(self, local_shard) -> int:
+        p = C.c_void_p()
+        self.L.check(self.L.lib.spmx_mg_y_shard(self.h, local_shard, C.byref(p)))
+        return p.value or 0
+
+    def allgather_y(self) -> float:
+        ms = C.c_float()
+        self.L.check(self.L.lib.spmx_mg_allgather_y(self.h, C.byref(ms)))
+        return ms.value
+
+    def y_full_ptr(self, local_rank=0) -> int:
+        p = C.c_void_p()
+        self.L.check(self.L.lib.spmx_mg_y_full(self.h, local_rank, C.byref(p)))
+        return p.value or 0
+
+    def allreduce(self, values, op="sum"):
+        vals = [float(v) for v in np.atleast_1d(values)]
+        arr = (C.c_double * len(vals))(*vals)
+        self.L.check(self.L.lib.spmx_mg_allreduce(self.h, arr, len(vals), {"sum": 0, "max": 1}[op]))
+        return list(arr)
+
+    def synchronize(self):
+        self.L.check(self.L.lib.spmx_mg_synchronize(self.h))

@@ -14,6 +14,7 @@
 #include <cstdlib>
 #include <cstring>
 #include <exception>
+#include <mutex>
 #include <new>
 #include <stdexcept>
 #include <string>
@@ -22,6 +23,7 @@
 #include "spmx_jit.cuh"
 #include "spmx_kernels.cuh"
 #include "spmx_partition.cuh"
+#include "spmx_probe.cuh"
 
 using spmx_dev::u64;
 
@@ -1230,6 +1232,45 @@ int spmx_max_relative_error(spmx_ctx* ctx, const float* d_y, const float* d_ref,
   });
 }
 
+int spmx_probe_l2_to_sm(spmx_ctx* ctx, int repeats, double* out_tbs, double* out_ms) {
+  return guarded([&] {
+    check(ctx);
+    if (repeats < 1) repeats = 1;
+    constexpr size_t kBytes = 64u << 20;  // resident in the 126 MB L2
+    constexpr int kWarpsPerSm = 32, kSteps = 2048;
+    float4* buf = (float4*)dev_alloc<char>(kBytes);
+    float* sink = dev_alloc<float>(1);
+    try {
+      CUDA_CHECK(cudaMemsetAsync(buf, 0, kBytes, ctx->stream));
+      const int ctas = ctx->sm_count * kWarpsPerSm / 4;
+      for (int w = 0; w < 3; ++w) {
+        spmx_dev::l2_rows_probe_kernel<<<ctas, 128, 0, ctx->stream>>>(buf, kBytes / 256, kSteps, w, sink);
+        post_launch();
+      }
+      float best = 1e30f;
+      for (int r = 0; r < repeats; ++r) {
+        CUDA_CHECK(cudaEventRecord(ctx->ev0, ctx->stream));
+        spmx_dev::l2_rows_probe_kernel<<<ctas, 128, 0, ctx->stream>>>(buf, kBytes / 256, kSteps, 10 + r, sink);
+        post_launch();
+        CUDA_CHECK(cudaEventRecord(ctx->ev1, ctx->stream));
+        CUDA_CHECK(cudaEventSynchronize(ctx->ev1));
+        float ms = 0.f;
+        CUDA_CHECK(cudaEventElapsedTime(&ms, ctx->ev0, ctx->ev1));
+        best = std::min(best, ms);
+      }
+      const double bytes = (double)ctas * 128 * kSteps * 16;
+      if (out_tbs) *out_tbs = bytes / (best * 1e-3) / 1e12;
+      if (out_ms) *out_ms = best;
+    } catch (...) {
+      cudaFree(buf);
+      cudaFree(sink);
+      throw;
+    }
+    CUDA_CHECK(cudaFree(buf));
+    CUDA_CHECK(cudaFree(sink));
+  });
+}
+
 int spmx_jit_available(void) { return spmx_jit::Nvrtc::get().ok() ? 1 : 0; }
 
 int spmx_jit_stats(uint64_t* kernels_compiled, double* seconds) {
@@ -1261,3 +1302,5 @@ int spmx_checksum_device(spmx_ctx* ctx, const float* d_y, size_t count, uint64_t
 }
 
 }  // extern "C"
+
+#include "spmx_mg.cuh"
