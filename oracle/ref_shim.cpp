@@ -4,7 +4,7 @@
 // is our own code; it includes the reference's public headers from where they
 // lie (/root/reference/proj/include, plus the header-only test generators in
 // /root/reference/proj/tests/oracles.hpp) and is compiled together with the
-// reference's own .cpp files by oracle/build_ref.sh into
+// reference's own .cpp files by oracle/Makefile, target `ref` into
 // oracle/_ref/libspmx_ref.so. No reference source is copied into this repo.
 //
 // Purpose: (1) pin oracle/spmx_oracle.c against the real thing, (2) generate the

@@ -9,7 +9,7 @@
  * Parity status: PINNED. Every function below is checked (tests/test_oracle_*.py)
  * against (a) the reference's own golden vectors restated in tests/golden/ and
  * (b) outputs of the unmodified reference library compiled from
- * /root/reference/proj/src into oracle/_ref/libspmx_ref.so (oracle/build_ref.sh).
+ * /root/reference/proj/src into oracle/_ref/libspmx_ref.so (oracle/Makefile, target `ref`).
  *
  * Each function cites the reference file:line it follows
  * (paths relative to /root/reference/proj).

@@ -222,7 +222,14 @@ struct RunConfig {
   bool verify = false;
   unsigned trials = 1;
   bool collect_counters = false;
-  int device = 0;          // extension: which GPU
+  int device = 0;          // extension: which GPU (the first one when gpus > 1)
+  unsigned gpus = 1;       // extension: row-shard A over GPUs device .. device+gpus-1 through the
+                           // library's multi-GPU driver (spmx_mg_*): the reference's fork-join over
+                           // RowRanges (executor.cpp:66-99) with GPUs for workers, ranges from
+                           // split_nnz(A, gpus) (partition.cpp:35-51); X replicated by one NCCL
+                           // broadcast, Y row-sharded. The Strategy divides every shard again.
+  unsigned shards = 0;     // extension: row blocks (0 = one per GPU; more puts several on a GPU)
+  bool shard_by_merge = false;  // extension: split_merge(A, gpus) instead of split_nnz
   bool jit_width = true;   // extension: compile the kernel for exactly X.cols at run time (NVRTC,
                            // cached per d; d = 32/64/128 are precompiled), the counterpart of the
                            // reference's per-d code generation behind Backend::Native. Ignored
@@ -238,6 +245,9 @@ struct RunReport {
   unsigned threads = 0;
   std::optional<double> max_rel_err;  // when verify is set
   uint64_t n_chunks = 0;              // extension: size of the device work list
+  unsigned gpus = 1;                  // extension: GPUs that shared the rows
+  double x_broadcast_s = 0.0;         // extension: the one NCCL broadcast of X (gpus > 1)
+  std::vector<RowRange> shard_rows;   // extension: the row block of every shard (gpus > 1)
 };
 
 inline constexpr double kVerifyTolerance = 1e-5;
@@ -285,6 +295,71 @@ inline DenseMatrix spmm_reference(const CsrMatrix& a, const DenseMatrix& x) {
   return y;
 }
 
+namespace detail {
+
+struct Mg {
+  spmx_mg* h = nullptr;
+  ~Mg() { if (h) spmx_mg_destroy(h); }
+};
+
+// run_spmm over several GPUs (RunConfig.gpus > 1 or shards > 1): same contract, the rows of A
+// divided among the GPUs first. Times are the max over GPUs of each GPU's own device time.
+inline std::pair<DenseMatrix, RunReport> run_spmm_multi(const CsrMatrix& a, const DenseMatrix& x,
+                                                        const RunConfig& cfg, bool dynamic,
+                                                        unsigned flags) {
+  if (a.row_ptr.size() != size_t(a.m) + 1)
+    throw std::invalid_argument("invalid CSR: row_ptr length != m+1");
+  if (a.col_indices.size() != size_t(a.nnz) || a.vals.size() != size_t(a.nnz))
+    throw std::invalid_argument("invalid CSR: col_indices/vals length != nnz");
+  const unsigned gpus = std::max(cfg.gpus, 1u);
+  std::vector<int> devices(gpus);
+  for (unsigned g = 0; g < gpus; ++g) devices[g] = cfg.device + int(g);
+  Mg mg;
+  check(spmx_mg_create(int(gpus), devices.data(), int(cfg.shards), &mg.h));
+  int n_shards = 0;
+  check(spmx_mg_info(mg.h, nullptr, nullptr, &n_shards, nullptr, nullptr));
+  std::vector<uint64_t> flat(2 * size_t(n_shards));
+  check(spmx_mg_shard_host(mg.h, a.m, a.n, a.nnz, a.row_ptr.data(), a.col_indices.data(), a.vals.data(),
+                           cfg.shard_by_merge ? SPMX_SHARD_BY_MERGE : SPMX_SHARD_BY_NNZ, flat.data()));
+  const int64_t d = x.cols;
+  float h2d_ms = 0.f, bcast_ms = 0.f;
+  check(spmx_mg_broadcast_x_host(mg.h, x.data.data(), 0, x.rows, d, &h2d_ms, &bcast_ms));
+
+  RunReport report;
+  report.gpus = gpus;
+  report.x_broadcast_s = double(bcast_ms) * 1e-3;
+  report.shard_rows = to_ranges(flat);
+  {
+    const double t0 = now_s();
+    check(spmx_mg_plan(mg.h, to_c(cfg.strategy), cfg.threads, dynamic ? 1 : 0, cfg.batch_size, flags));
+    check(spmx_mg_synchronize(mg.h));
+    report.codegen_s = now_s() - t0;
+  }
+  report.threads = cfg.threads;
+  if (flags & SPMX_JIT_WIDTH) {  // run-time code generation happens on the first launch for this d
+    double before = 0.0, after = 0.0;
+    check(spmx_jit_stats(nullptr, &before));
+    check(spmx_mg_spmm(mg.h, 1, nullptr, nullptr));
+    check(spmx_jit_stats(nullptr, &after));
+    report.codegen_s += after - before;
+  }
+  for (unsigned trial = 0; trial < cfg.trials; ++trial) {
+    float ms = 0.0f;
+    check(spmx_mg_spmm(mg.h, 1, &ms, nullptr));
+    report.times_s.push_back(double(ms) * 1e-3);
+  }
+  double sum = 0.0;
+  for (double t : report.times_s) sum += t;
+  report.mean_s = sum / double(report.times_s.size());
+  report.gflops = report.mean_s > 0.0 ? 2.0 * double(a.nnz) * double(d) / report.mean_s / 1e9 : 0.0;
+  DenseMatrix y(a.m, d);
+  check(spmx_mg_download_y(mg.h, y.data.data()));
+  if (cfg.verify) report.max_rel_err = max_relative_error(y, spmm_reference(a, x));
+  return {std::move(y), std::move(report)};
+}
+
+}  // namespace detail
+
 // executor.hpp:44-45
 inline std::pair<DenseMatrix, RunReport> run_spmm(const CsrMatrix& a, const DenseMatrix& x,
                                                   const RunConfig& cfg) {
@@ -298,6 +373,8 @@ inline std::pair<DenseMatrix, RunReport> run_spmm(const CsrMatrix& a, const Dens
   const bool jit = cfg.jit_width && spmx_jit_available() != 0;
   const unsigned flags = (cfg.backend == Backend::Interp ? SPMX_EXACT_ORDER : 0u) |
                          (jit ? SPMX_JIT_WIDTH : 0u);
+
+  if (cfg.gpus > 1 || cfg.shards > 1) return detail::run_spmm_multi(a, x, cfg, dynamic, flags);
 
   detail::Ctx& c = detail::thread_ctx(cfg.device);
   detail::DevCsr da(c, a);

@@ -258,10 +258,53 @@ static void executor_cases() {
   }
 }
 
+// RunConfig.gpus / shards: the same run_spmm call through the library's multi-GPU driver. On this
+// one-GPU box the row blocks of split_nnz(A, S) / split_merge(A, S) all live on device 0; the
+// result must not depend on how the rows were divided (test_executor.cpp:67-87 one level up).
+static void multi_gpu_cases() {
+  std::printf("multi-GPU driver through run_spmm (row blocks on one device)\n");
+  std::mt19937_64 rng(77);
+  CsrMatrix a = random_rect(3000, 900, 0.02, rng);
+  DenseMatrix x = random_dense(a.n, 45, 5);
+  DenseMatrix fused(a.m, 45), unfused(a.m, 45);
+  oracle_spmm_fused(a.m, a.n, a.row_ptr.data(), a.col_indices.data(), a.vals.data(), x.data.data(), a.n, 45,
+                    fused.data.data(), 1, nullptr);
+  oracle_spmm_unfused(a.m, a.n, a.row_ptr.data(), a.col_indices.data(), a.vals.data(), x.data.data(), a.n, 45,
+                      unfused.data.data());
+  const uint64_t want = oracle_checksum(fused.data.data(), fused.data.size());
+  for (unsigned shards : {2u, 5u, 8u})
+    for (bool by_merge : {false, true})
+      for (const RunConfig& base : all_configs(Backend::Interp, 4)) {
+        RunConfig cfg = base;
+        cfg.gpus = 1;
+        cfg.shards = shards;
+        cfg.shard_by_merge = by_merge;
+        cfg.trials = 2;
+        auto [y, rep] = run_spmm(a, x, cfg);
+        CHECK(checksum(y) == want);
+        CHECK(rep.times_s.size() == 2 && rep.gpus == 1 && rep.shard_rows.size() == shards);
+        std::vector<uint64_t> flat(2 * size_t(shards));
+        if (by_merge) oracle_split_merge(uint64_t(a.m), uint64_t(a.nnz), a.row_ptr.data(), shards, flat.data());
+        else oracle_split_nnz(uint64_t(a.m), uint64_t(a.nnz), a.row_ptr.data(), shards, flat.data());
+        for (unsigned t = 0; t < shards; ++t)
+          CHECK(rep.shard_rows[t].begin == flat[2 * t] && rep.shard_rows[t].end == flat[2 * t + 1]);
+        cfg.backend = Backend::Native;
+        cfg.verify = true;
+        auto [y2, rep2] = run_spmm(a, x, cfg);
+        CHECK(rep2.max_rel_err && *rep2.max_rel_err <= kVerifyTolerance);
+        CHECK(max_relative_error(y2, unfused) <= kVerifyTolerance);
+      }
+  RunConfig bad;
+  bad.gpus = 64;  // more GPUs than the box has
+  bad.dynamic_dispatch = false;
+  CHECK_THROWS_AS(run_spmm(a, x, bad), std::invalid_argument);
+}
+
 int main() {
   try {
     partition_cases();
     executor_cases();
+    multi_gpu_cases();
   } catch (const std::exception& e) {
     std::printf("unexpected exception: %s\n", e.what());
     return 2;

@@ -7,7 +7,7 @@
 //                   [--cols D] [--strategy row|nnz|merge] [--dispatch static|dynamic]
 //                   [--backend native|interp] [--threads T] [--batch-size B] [--trials K]
 //                   [--seed S] [--verify] [--no-jit] [--format json|csv] [--report FILE]
-//                   [--save-cache f.jspm] [--peak-gbs G]
+//                   [--save-cache f.jspm] [--peak-gbs G] [--gpus G] [--shards S] [--shard-by nnz|merge]
 //   spmx_bench_b200 sweep [common options] [--d-list 16 32 ...] [--strategies row nnz merge]
 //                   [--backends native interp] [--dispatch static|dynamic]
 //
@@ -44,6 +44,8 @@ struct Cli {
   bool verify = false, jit = true;
   std::string format = "json", report_path, save_cache_path;
   double peak_gbs = 6551.0;  // measured HBM copy peak of this pool's B200s (MEASURED_PEAKS.json)
+  unsigned gpus = 1, shards = 0;  // row-shard A over G GPUs (the library's multi-GPU driver)
+  std::string shard_by = "nnz";
   bool sweep = false;
   std::vector<int> d_list{16, 32};
   std::vector<std::string> strategies{"row", "nnz", "merge"}, backends{"native", "interp"};
@@ -124,6 +126,10 @@ RunConfig make_run_config(const Cli& c) {
   cfg.verify = c.verify;
   cfg.trials = c.trials;
   cfg.jit_width = c.jit;
+  cfg.gpus = c.gpus;
+  cfg.shards = c.shards;
+  if (c.shard_by != "nnz" && c.shard_by != "merge") throw UsageError("--shard-by: expected nnz or merge");
+  cfg.shard_by_merge = c.shard_by == "merge";
   return cfg;
 }
 
@@ -169,7 +175,16 @@ Row report_row(const std::string& matrix, const CsrMatrix& a, int d, const RunCo
   r.num("gbs", rep.mean_s > 0 ? bytes / rep.mean_s / 1e9 : 0.0);
   r.num("roofline_frac", rep.mean_s > 0 ? bytes / rep.mean_s / 1e9 / peak_gbs : 0.0);
   r.u64("n_chunks", rep.n_chunks);
-  r.integer("gpus", 1);
+  r.integer("gpus", rep.gpus);
+  if (rep.gpus > 1 || !rep.shard_rows.empty()) {
+    r.num("x_broadcast_s", rep.x_broadcast_s);
+    r.num("roofline_frac_all_gpus", rep.mean_s > 0 ? bytes / rep.mean_s / 1e9 / (peak_gbs * rep.gpus) : 0.0);
+    std::string sr = "[";
+    for (size_t i = 0; i < rep.shard_rows.size(); ++i)
+      sr += std::string(i ? ", " : "") + "[" + std::to_string(rep.shard_rows[i].begin) + ", " +
+            std::to_string(rep.shard_rows[i].end) + "]";
+    r.kv.emplace_back("shard_rows", sr + "]");
+  }
   return r;
 }
 
@@ -285,6 +300,9 @@ Cli parse(int argc, char** argv) {
     else if (key == "--report") c.report_path = value();
     else if (key == "--peak-gbs") c.peak_gbs = std::atof(value().c_str());
     else if (key == "--dispatch") c.dispatch = value();
+    else if (key == "--gpus") c.gpus = unsigned(positive(value()));
+    else if (key == "--shards") c.shards = unsigned(positive(value()));
+    else if (key == "--shard-by") c.shard_by = value();
     else if (!c.sweep && key == "--cols") c.cols = int(positive(value()));
     else if (!c.sweep && key == "--strategy") c.strategy = value();
     else if (!c.sweep && key == "--backend") c.backend = value();
