@@ -63,6 +63,13 @@ extern "C" {
                                counterpart of the reference's per-d code generation
                                (plan.cpp:80-93, jit.cpp:136-154). d = 32/64/128 are precompiled. */
 
+#define SPMX_CLAIM_KERNEL 8u /* dynamic plans only: run the literal form of the reference's dynamic
+                               dispatch (persistent warps claim `batch` rows at a time from a device
+                               counter, rows never cut) in the default mode too. Exact-order dynamic
+                               plans always do. Without it a default-mode dynamic plan is served by
+                               the row-split work list, whose chunks the hardware hands to the SMs
+                               as they free up (and whose long rows are shared between chunks). */
+
 typedef struct spmx_ctx spmx_ctx;   /* one per (device, stream) */
 typedef struct spmx_csr spmx_csr;   /* A resident on the device */
 typedef struct spmx_plan spmx_plan; /* partition of A for one (strategy, parts, flags) */
@@ -131,8 +138,9 @@ int spmx_next_batch_claims(spmx_ctx* ctx, uint64_t m, uint64_t batch, size_t n_c
 
 /* ---- plan: make_partition(A, strategy, T, dynamic, batch) (partition.cpp:86-104) plus the
  *      device work list derived from it. parts == 0 picks a default that fills the GPU.
- *      dynamic != 0 (row-split only, else SPMX_EINVAL) makes persistent CTAs claim `batch` rows
- *      at a time from a device counter, the analogue of DispatchCounter (partition.hpp:38-40). */
+ *      dynamic != 0 (row-split only, else SPMX_EINVAL; no RowRange list, as in the reference)
+ *      asks for dynamic dispatch, the analogue of DispatchCounter (partition.hpp:38-40): see
+ *      SPMX_CLAIM_KERNEL for how it runs. */
 int spmx_plan_create(spmx_ctx* ctx, const spmx_csr* a, int strategy, unsigned parts, int dynamic,
                      uint64_t batch, unsigned flags, spmx_plan** out);
 int spmx_plan_destroy(spmx_plan* p);

@@ -27,6 +27,7 @@ ROW, NNZ, MERGE = 0, 1, 2
 STRATEGY = {"row": ROW, "nnz": NNZ, "merge": MERGE}
 EXACT_ORDER = 1
 JIT_WIDTH = 4
+CLAIM_KERNEL = 8
 
 NVCC_FLAGS = ["-gencode", "arch=compute_100a,code=sm_100a", "-lineinfo", "-O3", "-std=c++17",
               "-Xcompiler", "-fPIC", "-shared"]

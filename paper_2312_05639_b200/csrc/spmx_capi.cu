@@ -129,7 +129,8 @@ struct spmx_plan {
   int strategy = 0;
   unsigned parts = 0;
   unsigned flags = 0;
-  bool dynamic = false;
+  bool dynamic = false;  // make_partition's dynamic dispatch was asked for (no RowRange list)
+  bool claims = false;   // ... and it runs as the atomic-claim kernel (see plan_build)
   u64 batch = 128;
   u64 n_chunks = 0;
   u64* ranges = nullptr;     // 2*parts, device (absent under dynamic dispatch)
@@ -274,7 +275,7 @@ void validate_on_device(spmx_ctx* ctx, const spmx_csr* a) {
 // ---- kernel dispatch per d ------------------------------------------------------------------
 template <int D_CT, int G, int VEC, int NT, bool RAGGED>
 void launch_one(const spmx_plan* p, const spmx_dev::SpmmArgs& args, cudaStream_t st, int sm_count) {
-  if (p->dynamic) {
+  if (p->claims) {
     int occ = 0;
     CUDA_CHECK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(
         &occ, spmx_dev::spmm_dynamic_kernel<D_CT, G, VEC, NT, RAGGED>, spmx_dev::kWarpsPerCta * 32,
@@ -307,6 +308,8 @@ void launch_one(const spmx_plan* p, const spmx_dev::SpmmArgs& args, cudaStream_t
   post_launch();
 }
 
+// runtime-d kernels (ragged tiles): the shape spmx_jit::choose_shape picks for the slab, with the
+// tile count rounded up to the next instantiated one (1, 2, 4; 8 with all 32 lanes)
 template <int VEC>
 void launch_generic(const spmx_plan* p, const spmx_dev::SpmmArgs& a, int g, int nt,
                     cudaStream_t st, int sms) {
@@ -316,23 +319,21 @@ void launch_generic(const spmx_plan* p, const spmx_dev::SpmmArgs& a, int g, int 
       case 2: return launch_one<0, 2, VEC, 1, true>(p, a, st, sms);
       case 4: return launch_one<0, 4, VEC, 1, true>(p, a, st, sms);
       case 8: return launch_one<0, 8, VEC, 1, true>(p, a, st, sms);
-      case 16: return launch_one<0, 16, VEC, 1, true>(p, a, st, sms);
-      case 32: return launch_one<0, 32, VEC, 1, true>(p, a, st, sms);
     }
+  } else if (g == 8) {
+    switch (nt) {
+      case 2: return launch_one<0, 8, VEC, 2, true>(p, a, st, sms);
+      case 4: return launch_one<0, 8, VEC, 4, true>(p, a, st, sms);
+    }
+  } else if (g == 16 && nt == 4) {
+    return launch_one<0, 16, VEC, 4, true>(p, a, st, sms);
   } else if (g == 32) {
     switch (nt) {
-      case 2: return launch_one<0, 32, VEC, 2, true>(p, a, st, sms);
       case 4: return launch_one<0, 32, VEC, 4, true>(p, a, st, sms);
       case 8: return launch_one<0, 32, VEC, 8, true>(p, a, st, sms);
     }
   }
   throw std::runtime_error("internal: no kernel for this shape");
-}
-
-int pow2_ceil(int v) {
-  int p = 1;
-  while (p < v) p <<= 1;
-  return p;
 }
 
 // carry_out buffer of the plan for width d (cudaMalloc/cudaFree synchronise the device, so
@@ -400,10 +401,20 @@ void run_kernels(spmx_ctx* ctx, const spmx_plan* p, const spmx_csr* a, const flo
                  int64_t d, float* d_y, cudaStream_t st, u64 cb, u64 ce, const int* abort_flag,
                  u64 first_lo = 0, u64 first_hi = kNoLimit, bool fixup_only = false) {
   if (a->m == 0) return;
-  if (!p->dynamic && ce <= cb) return;  // empty block of the host pipeline
+  if (!p->claims && ce <= cb) return;  // empty block of the host pipeline
+  // widest column vector the alignment of X and Y rows allows
   const bool aligned16 = ((uintptr_t)d_x % 16 == 0) && ((uintptr_t)d_y % 16 == 0);
-  const int vec = (d % 4 == 0 && aligned16) ? 4 : 1;
-  const int slab_max = 32 * vec * 8;  // G=32, NT=8
+  const int vec_max = (d % 4 == 0 && aligned16) ? 4 : 1;
+  // Narrow rows: eight lanes with narrower vectors beat fewer lanes with float4 (eight positions
+  // in flight per group, column/value broadcast through shared memory, four instead of eight
+  // chunk streams per warp: d = 16 178 -> 130 us, d = 8 207 -> 117 us on c2's matrix), so the
+  // vector is narrowed until a row spans at least five lanes.
+  const int vec = spmx_jit::narrow_vec((int)d, vec_max);
+  // Columns per launch. Wider matrices are multiplied slab by slab (A is streamed again per
+  // slab: 8 bytes per nonzero against 4 * 128 gathered). With float4 columns the slab is 128
+  // wide, the shape of the d = 128 kernel (8 lanes x 4 tiles, measured best; one launch over
+  // 256 columns with 16-lane groups took 1.30 ms on c2's matrix against 1.05 ms for two slabs).
+  const int slab_max = vec == 4 ? 128 : 32 * vec * 8;
 
   ensure_carry(p, d);
 
@@ -427,11 +438,12 @@ void run_kernels(spmx_ctx* ctx, const spmx_plan* p, const spmx_csr* a, const flo
   // run-time instantiation for exactly this d (SPMX_JIT_WIDTH): one launch covers the whole
   // width when it fits 32 lanes x 8 tiles; the precompiled widths and dynamic plans keep
   // their own kernels
-  const bool precompiled = vec == 4 && (d == 32 || d == 64 || d == 128);
-  if ((p->flags & SPMX_JIT_WIDTH) && !p->dynamic && !precompiled && d <= spmx_jit::max_width(vec)) {
+  const bool precompiled = (vec == 4 && (d == 32 || d == 64 || d == 128)) || (vec == 2 && d == 16) ||
+                           (vec == 1 && d == 8);
+  if ((p->flags & SPMX_JIT_WIDTH) && !p->claims && !precompiled && d <= spmx_jit::max_width(vec_max)) {
     int dev = 0;
     CUDA_CHECK(cudaGetDevice(&dev));
-    const spmx_jit::Kernel& k = spmx_jit::get(dev, (int)d, vec);
+    const spmx_jit::Kernel& k = spmx_jit::get(dev, (int)d, vec_max);
     args.c0 = 0;
     args.dw = (int)d;
     const int chunks_per_cta = spmx_dev::kWarpsPerCta * (32 / k.shape.g);
@@ -453,24 +465,38 @@ void run_kernels(spmx_ctx* ctx, const spmx_plan* p, const spmx_csr* a, const flo
     const int dw = (int)std::min<int64_t>(slab_max, d - c0);
     args.c0 = (int)c0;
     args.dw = dw;
-    if (p->dynamic && !fixup_only) CUDA_CHECK(cudaMemsetAsync(p->counter, 0, sizeof(u64), st));
+    if (p->claims && !fixup_only) CUDA_CHECK(cudaMemsetAsync(p->counter, 0, sizeof(u64), st));
 #ifndef SPMX_NT
 #define SPMX_NT 2  // float4 tiles per lane for the specialised widths
 #endif
     if (fixup_only) {
     } else if (vec == 4 && c0 == 0 && d == 32) {
-      launch_one<32, 8, 4, 1, false>(p, args, st, ctx->sm_count);  // see Tune<32, 1>
+      launch_one<32, 8, 4, 1, false>(p, args, st, ctx->sm_count);  // 8 lanes x float4
     } else if (vec == 4 && c0 == 0 && d == 64) {
       launch_one<64, 16 / SPMX_NT, 4, SPMX_NT, false>(p, args, st, ctx->sm_count);
+    } else if (vec == 2 && c0 == 0 && d == 16) {
+      launch_one<16, 8, 2, 1, false>(p, args, st, ctx->sm_count);  // 8 lanes x float2
+    } else if (vec == 1 && c0 == 0 && d == 8) {
+      launch_one<8, 8, 1, 1, false>(p, args, st, ctx->sm_count);
     } else if (vec == 4 && c0 == 0 && d == 128) {
-      launch_one<128, 8, 4, 4, false>(p, args, st, ctx->sm_count);  // see Tune<128, 4>
+      launch_one<128, 8, 4, 4, false>(p, args, st, ctx->sm_count);  // 8 lanes x 4 tiles
+    } else if (vec == 4 && dw == 128) {
+      launch_one<0, 8, 4, 4, false>(p, args, st, ctx->sm_count);  // full slab of a wider matrix
     } else {
       const int lanes = (dw + vec - 1) / vec;
-      int g = pow2_ceil(std::min(lanes, 32));
-      int nt = 1;
-      if (lanes > 32) nt = pow2_ceil((lanes + 31) / 32);
+      int g = 1, nt = 1;
+      while (g < 8 && g < lanes) g <<= 1;
+      for (;; g <<= 1) {  // 8 lanes up to 4 tiles, 16 lanes x 4, 32 lanes x 4 or 8 (slab_max bounds it)
+        nt = (lanes + g - 1) / g;
+        if (nt <= (g < 32 ? 4 : 8)) break;
+      }
+      nt = nt <= 2 ? nt : nt <= 4 ? 4 : 8;
+      if (g == 16) nt = 4;
+      if (g == 32 && nt < 4) nt = 4;
       if (vec == 4)
         launch_generic<4>(p, args, g, nt, st, ctx->sm_count);
+      else if (vec == 2)
+        launch_one<0, 8, 2, 1, true>(p, args, st, ctx->sm_count);  // d = 12 (16 is precompiled)
       else
         launch_generic<1>(p, args, g, nt, st, ctx->sm_count);
     }
@@ -528,7 +554,15 @@ spmx_plan* plan_build(spmx_ctx* ctx, const spmx_csr* a, int strategy, unsigned p
     p->flags = flags;
     p->dynamic = dynamic != 0;
     p->batch = batch ? batch : 128;
-    if (p->dynamic) {
+    // Dynamic row dispatch (DispatchCounter, partition.hpp:38-40: workers claim `batch` rows at a
+    // time). Exact-order plans and SPMX_CLAIM_KERNEL run it literally: persistent warps claim
+    // row batches with atomics (spmm_dynamic_kernel), rows are never cut. In the default mode the
+    // same request is served by the row-split work list below: its chunks ARE handed to the SMs
+    // dynamically, by the hardware's CTA scheduler, and long rows can be shared between chunks
+    // (the claim kernel is row-granular: one lane group walks c2's 39 542-nonzero row alone,
+    // 7.4 ms against 0.26 ms).
+    p->claims = p->dynamic && (exact || (flags & SPMX_CLAIM_KERNEL));
+    if (p->claims) {
       p->counter = dev_alloc_async<u64>(ctx, 1);
       CUDA_CHECK(cudaMemsetAsync(p->counter, 0, sizeof(u64), ctx->stream));
       return p;
@@ -986,7 +1020,7 @@ int spmx_plan_chunks(const spmx_plan* p, uint64_t* out_row, uint64_t* out_nnz) {
   return guarded([&] {
     check(p);
     check(p->ctx);
-    if (p->dynamic) return;
+    if (p->claims) return;
     const size_t bytes = ((size_t)p->n_chunks + 1) * 8;
     CUDA_CHECK(cudaMemcpyAsync(out_row, p->chunk_row, bytes, cudaMemcpyDeviceToHost, p->ctx->stream));
     CUDA_CHECK(cudaMemcpyAsync(out_nnz, p->chunk_nnz, bytes, cudaMemcpyDeviceToHost, p->ctx->stream));
@@ -1102,7 +1136,7 @@ int spmx_spmm_host(spmx_ctx* ctx, int64_t m, int64_t n, int64_t nnz, const uint6
       // blocks = runs of whole chunks with about equal nonzero counts
       int nblocks = 1;
       std::vector<u64> cb{0, plan->n_chunks}, row_b{0, (u64)m}, nnz_b{0, (u64)nnz};
-      if (!plan->dynamic && plan->n_chunks >= 64 && nnz > (1 << 20)) {
+      if (!plan->claims && plan->n_chunks >= 64 && nnz > (1 << 20)) {
         nblocks = (int)std::min<u64>(kMaxBlocks, std::max<u64>(2, env_u64("SPMX_HOST_BLOCKS", 8)));
         cb.assign(nblocks + 1, 0);
         row_b.assign(nblocks + 1, 0);

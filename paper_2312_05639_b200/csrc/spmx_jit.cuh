@@ -65,21 +65,34 @@ struct Shape {
   bool ragged;
 };
 
-// lanes per row and tiles per lane for width d: the fewest lanes (but at least 4, or the whole
-// row when it is narrower: one- and two-lane groups gather uncoalesced) that keep <= 4 tiles
-// per lane (more row groups per warp), then <= 8 tiles with all 32 lanes. d beyond that is
-// slabbed by the caller.
-inline Shape choose_shape(int d, int vec) {
+// Column vector per lane for width d: the widest of {4, 2, 1} floats that the alignment allows
+// (vec_max) and that still spreads a row over at least five lanes, i.e. an 8-lane group with
+// eight positions in flight (see run_kernels); rows of fewer than five columns use scalars.
+inline int narrow_vec(int d, int vec_max) {
+  for (int v = vec_max; v > 1; v >>= 1)
+    if (d % v == 0 && d / v >= 5) return v;
+  return 1;
+}
+
+// lanes per row and tiles per lane for width d: eight lanes whenever the row fits four tiles per
+// lane (a row of fewer than five vectors: the next power of two), else 16, else all 32 lanes with
+// up to eight tiles. Eight-lane groups measured best at every width they can hold (four chunk
+// streams per warp, eight positions per batch, column/value broadcast through shared memory):
+// d = 48 runs 8 x 2 (ragged) instead of 4 x 3, d = 20 8 x 1 instead of 4 x 2. d beyond 32 x 8
+// vectors is slabbed by the caller.
+inline Shape choose_shape(int d, int vec_max) {
+  const int vec = narrow_vec(d, vec_max);
   const int lanes = (d + vec - 1) / vec;
-  int gmin = 1;
-  while (gmin < 4 && gmin < lanes) gmin <<= 1;
-  for (int g = gmin; g <= 32; g <<= 1) {
+  int g = 1;
+  while (g < 8 && g < lanes) g <<= 1;
+  for (; g <= 32; g <<= 1) {
     const int nt = (lanes + g - 1) / g;
     if (nt <= (g < 32 ? 4 : 8)) return {g, vec, nt, g * nt * vec != d};
   }
   return {32, vec, 8, true};
 }
-inline int max_width(int vec) { return 32 * 8 * vec; }
+// widest d compiled as one kernel (wider ones run as slabs of the precompiled shapes)
+inline int max_width(int vec) { return vec == 4 ? 128 : 32 * 8 * vec; }
 
 struct Kernel {
   cudaLibrary_t lib = nullptr;

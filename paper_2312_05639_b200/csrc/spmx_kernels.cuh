@@ -255,29 +255,21 @@ __device__ __forceinline__ void zero_acc_from(float (&acc)[NT][VEC], float zero)
 #endif
 constexpr int kStageBatch = SPMX_STAGE_BATCH;
 
-// Per-width tuning (measured on B200, tools/dev_bench.py): CTAs per SM the register budget is
-// set for, and LDG.128 gathers in flight per lane. Narrow rows (d = 32: one 128-byte line per
-// row) do better with more resident warps and a shallower pipeline.
-template <int D_CT, int NT>
+// Per-shape tuning (measured on B200, tools/dev_bench.py): CTAs per SM the register budget is
+// set for, and row gathers in flight per lane.
+//   8 lanes x 1 tile  (d = 8, 16, 32 and every width of 5..8 vectors): one load per position and
+//                     lane, so more resident warps (24 per SM) and a pipeline as deep as a batch;
+//   8 lanes x 2..4 tiles (d = 64, 128, 33..128 in general): 16 loads in flight per lane, 16 warps;
+//   wider groups / more tiles (runtime-d slabs): as measured in round 1.
+template <int D_CT, int G, int NT>
 struct Tune {
 #ifdef SPMX_MIN_CTAS_RAW
   static constexpr int kMinCtas = SPMX_MIN_CTAS_RAW;
 #else
-  static constexpr int kMinCtas = ((NT <= 2) ? SPMX_MIN_CTAS : 1) * (8 / kWarpsPerCta);
+  static constexpr int kMinCtas =
+      ((G == 8 && NT == 1) ? 3 : (NT <= 2 || (G == 8 && NT <= 4)) ? SPMX_MIN_CTAS : 1) * (8 / kWarpsPerCta);
 #endif
-  static constexpr int kInFlight = SPMX_U;
-};
-// d = 128: four float4 tiles per lane, 8 lanes per row (4 rows per warp step instead of 2:
-// fewer instructions per nonzero), same 16 loads in flight and 16 warps/SM.
-template <>
-struct Tune<128, 4> {
-  static constexpr int kMinCtas = SPMX_MIN_CTAS * (8 / kWarpsPerCta);
-  static constexpr int kInFlight = SPMX_U;
-};
-template <>
-struct Tune<32, 1> {
-  static constexpr int kMinCtas = 3 * (8 / kWarpsPerCta);
-  static constexpr int kInFlight = 8;
+  static constexpr int kInFlight = (G == 8 && NT == 1) ? 8 : SPMX_U;
 };
 
 __host__ __device__ constexpr int pipeline_depth(int want, int g) {
@@ -345,12 +337,28 @@ struct WarpScratch {
 // row is stored and the accumulators are zeroed. Every row that lies wholly inside a piece
 // is therefore ONE fmaf chain in CSR order: bitwise equal to the reference.
 // A piece must span fewer than 2^32 nonzeros (the plan guarantees it).
-template <int G, int VEC, int NT, bool RAGGED>
+// Does tile t of lane lg hold columns of the slab? Always, unless the slab is narrower than
+// G * NT * VEC (RAGGED). With a compile-time width the test folds away for every tile that lies
+// wholly inside (or outside) the row: only the one tile the row ends in keeps a lane predicate.
+template <int D_CT, int G, int VEC, bool RAGGED>
+__device__ __forceinline__ bool tile_on(const SpmmArgs& a, int t, int lg) {
+  if constexpr (!RAGGED) {
+    return true;
+  } else if constexpr (D_CT > 0) {
+    if ((t * G + G - 1) * VEC < D_CT) return true;
+    if (t * G * VEC >= D_CT) return false;
+    return (t * G + lg) * VEC < D_CT;
+  } else {
+    return (t * G + lg) * VEC < a.dw;
+  }
+}
+
+template <int D_CT, int G, int VEC, int NT, bool RAGGED>
 __device__ __forceinline__ void store_lane(const SpmmArgs& a, float* dst_lane, int lg,
                                            const float (&acc)[NT][VEC], u64 pol) {
 #pragma unroll
   for (int t = 0; t < NT; ++t)
-    if (!RAGGED || (t * G + lg) * VEC < a.dw) st_y<VEC>(dst_lane + t * G * VEC, acc[t], pol);
+    if (tile_on<D_CT, G, VEC, RAGGED>(a, t, lg)) st_y<VEC>(dst_lane + t * G * VEC, acc[t], pol);
 }
 
 template <int D_CT, int G, int VEC, int NT, bool RAGGED>
@@ -365,14 +373,14 @@ __device__ __forceinline__ void process_piece(const SpmmArgs& a, bool active, u6
   constexpr bool kRefillFirst = SPMX_REFILL_FIRST >= 0 ? (SPMX_REFILL_FIRST != 0) : (NT <= 2);
   // positions in flight per lane: the largest power of two with U * NT <= kInFlight, at most G
   // (so that U divides G and a position keeps its pipeline slot from batch to batch)
-  constexpr int U = pipeline_depth(Tune<D_CT, NT>::kInFlight / NT, G);
+  constexpr int U = pipeline_depth(Tune<D_CT, G, NT>::kInFlight / NT, G);
   const int g = lane / G, lg = lane % G;
   const int ldx = D_CT ? D_CT : a.ldx;
   // row r1 is staged too: clipped to the piece it is empty unless the piece ends inside it
   const u64 row_lim = active ? r1 + (r1 < a.m ? 1 : 0) : r0;
   const u32* __restrict__ colp = a.col + j0;
   const float* __restrict__ valp = a.vals + j0;
-  const int lane_col = a.c0 + lg * VEC;  // first column this lane owns
+  const int lane_col = (D_CT ? 0 : a.c0) + lg * VEC;  // first column this lane owns
   const float* __restrict__ xbase = a.x + lane_col;
   float* const carry_lane = carry_row ? carry_row + lane_col : nullptr;
   const u32 span = active ? (u32)(j1 - j0) : 0u;
@@ -389,7 +397,7 @@ __device__ __forceinline__ void process_piece(const SpmmArgs& a, bool active, u6
   if (carry_lane != nullptr && active && span == 0u && r1 < a.m) {
     float z[NT][VEC];
     zero_acc(z);
-    store_lane<G, VEC, NT, RAGGED>(a, carry_lane, lg, z, pol_first);
+    store_lane<D_CT, G, VEC, NT, RAGGED>(a, carry_lane, lg, z, pol_first);
   }
 
   u32 ws = 0;  // nonzero offset where the current window starts
@@ -436,7 +444,7 @@ __device__ __forceinline__ void process_piece(const SpmmArgs& a, bool active, u6
           const float* xr = xbase + (size_t)kq * (size_t)ldx;
 #pragma unroll
           for (int t = 0; t < NT; ++t)
-            if (!RAGGED || (t * G + lg) * VEC < a.dw) xv[u][t] = ld_x<VEC>(xr + t * G * VEC, pol_last);
+            if (tile_on<D_CT, G, VEC, RAGGED>(a, t, lg)) xv[u][t] = ld_x<VEC>(xr + t * G * VEC, pol_last);
         }
       }
     };
@@ -479,7 +487,7 @@ __device__ __forceinline__ void process_piece(const SpmmArgs& a, bool active, u6
         while (em) {
           const int src = (__ffs(em) - 1) - g * G;
           em &= em - 1;
-          store_lane<G, VEC, NT, RAGGED>(a, ywin + (size_t)(q0 + src) * (size_t)ldx, lg, acc, pol_first);
+          store_lane<D_CT, G, VEC, NT, RAGGED>(a, ywin + (size_t)(q0 + src) * (size_t)ldx, lg, acc, pol_first);
         }
       }
     }
@@ -555,7 +563,7 @@ __device__ __forceinline__ void process_piece(const SpmmArgs& a, bool active, u6
         if (t < rem) {
 #pragma unroll
           for (int tt = 0; tt < NT; ++tt)
-            if (!RAGGED || (tt * G + lg) * VEC < a.dw) {
+            if (tile_on<D_CT, G, VEC, RAGGED>(a, tt, lg)) {
               fma_tile<VEC, kPackFma>(vq, xv[u][tt], acc[tt]);
             }
         }
@@ -565,11 +573,11 @@ __device__ __forceinline__ void process_piece(const SpmmArgs& a, bool active, u6
           const float* xr = xbase + (size_t)kq * (size_t)ldx;
 #pragma unroll
           for (int tt = 0; tt < NT; ++tt)
-            if (!RAGGED || (tt * G + lg) * VEC < a.dw) xv[u][tt] = ld_x<VEC>(xr + tt * G * VEC, pol_last);
+            if (tile_on<D_CT, G, VEC, RAGGED>(a, tt, lg)) xv[u][tt] = ld_x<VEC>(xr + tt * G * VEC, pol_last);
         }
         if (t == e_rel) {  // row k ends here: store it, start the next one
           float* dst = (cur.y != kCarryIdx) ? ywin + (size_t)cur.y * (size_t)ldx : carry_lane;
-          store_lane<G, VEC, NT, RAGGED>(a, dst, lg, acc, pol_first);
+          store_lane<D_CT, G, VEC, NT, RAGGED>(a, dst, lg, acc, pol_first);
           zero_acc_from(acc, zero_f);
           ++k;
           e_rel = (k < count) ? (int)min((u32)e_rel + (nxt.x - cur.x), (u32)kNoRowEnd) : kNoRowEnd;
@@ -582,7 +590,7 @@ __device__ __forceinline__ void process_piece(const SpmmArgs& a, bool active, u6
           const float* xr = xbase + (size_t)kq * (size_t)ldx;
 #pragma unroll
           for (int tt = 0; tt < NT; ++tt)
-            if (!RAGGED || (tt * G + lg) * VEC < a.dw) xv[u][tt] = ld_x<VEC>(xr + tt * G * VEC, pol_last);
+            if (tile_on<D_CT, G, VEC, RAGGED>(a, tt, lg)) xv[u][tt] = ld_x<VEC>(xr + tt * G * VEC, pol_last);
         }
         vq = vq_n;
         kq = kq_n;
@@ -597,7 +605,7 @@ __device__ __forceinline__ void process_piece(const SpmmArgs& a, bool active, u6
 
 // Static work list: group s of the grid (G lanes) owns chunk s.
 template <int D_CT, int G, int VEC, int NT, bool RAGGED>
-__global__ void __launch_bounds__(kWarpsPerCta * 32, Tune<D_CT, NT>::kMinCtas)
+__global__ void __launch_bounds__(kWarpsPerCta * 32, Tune<D_CT, G, NT>::kMinCtas)
 spmm_chunk_kernel(const SpmmArgs a) {
   constexpr int NGW = 32 / G;
   __shared__ WarpScratch<G> scratch[kWarpsPerCta];
@@ -628,7 +636,7 @@ spmm_chunk_kernel(const SpmmArgs a) {
 // covering [0, m) exactly as the reference's dispatcher does; the claimed rows are dealt
 // to the warp's groups in contiguous runs of about equal nonzero count (rows are never split).
 template <int D_CT, int G, int VEC, int NT, bool RAGGED>
-__global__ void __launch_bounds__(kWarpsPerCta * 32, Tune<D_CT, NT>::kMinCtas)
+__global__ void __launch_bounds__(kWarpsPerCta * 32, Tune<D_CT, G, NT>::kMinCtas)
 spmm_dynamic_kernel(const SpmmArgs a) {
   constexpr int NGW = 32 / G;
   __shared__ WarpScratch<G> scratch[kWarpsPerCta];

@@ -29,8 +29,9 @@ import sys
 
 _INSTR = re.compile(r"\s+/\*([0-9a-f]{4,})\*/\s+(.*?);\s+/\* (0x[0-9a-f]{16}) \*/")
 _HI = re.compile(r"\s+/\* (0x[0-9a-f]{16}) \*/")
-# a row gather of the walk loop: 128-bit load through the read-only path
-_GATHER = re.compile(r"LDG\.E(\.\w+)*\.128\.CONSTANT")
+# a row gather of the walk loop: 128-bit load through the read-only path (64-bit for the d = 16
+# kernel, whose 8-lane groups read a 64-byte row as float2 per lane)
+_GATHERS = {128: re.compile(r"LDG\.E(\.\w+)*\.128\.CONSTANT"), 64: re.compile(r"LDG\.E(\.\w+)*\.64\.CONSTANT")}
 # branch with its target (plain, predicated, or uniform: "BRA.U !UP0, 0x23b0")
 _BRA = r"\bBRA(?:\.U)?\s+(?:!?UP\d+,\s*)?(0x[0-9a-f]+)"
 
@@ -161,9 +162,11 @@ def _free_store_barrier(body, sb, target):
     return edits
 
 
-def plan_patch(code, log=None):
-    """Returns a list of (instruction index, new hi word) or None when a precondition fails."""
+def plan_patch(code, log=None, width=128):
+    """Returns a list of (instruction index, new hi word) or None when a precondition fails.
+    width: bits per lane of the kernel's row gathers."""
     say = log or (lambda s: None)
+    _GATHER = _GATHERS[width]
     # the walk loop: the backward branch whose body holds the most 128-bit constant-path gathers
     best = None
     for i, ins in enumerate(code):
@@ -319,9 +322,14 @@ class SassSchedError(RuntimeError):
     """A precompiled width could not be re-scheduled (the preconditions no longer hold)."""
 
 
+# kernels whose 64-byte rows are gathered with 64-bit loads
+_NARROW = ("ILi16ELi8ELi2ELi1ELb0",)
+
+
 def patch_library(lib, kernels=("spmm_chunk_kernelILi64ELi8ELi4ELi2ELb0", "spmm_dynamic_kernelILi64ELi8ELi4ELi2ELb0",
                                 "spmm_chunk_kernelILi32ELi8ELi4ELi1ELb0", "spmm_dynamic_kernelILi32ELi8ELi4ELi1ELb0",
-                                "spmm_chunk_kernelILi128ELi8ELi4ELi4ELb0", "spmm_dynamic_kernelILi128ELi8ELi4ELi4ELb0"),
+                                "spmm_chunk_kernelILi128ELi8ELi4ELi4ELb0", "spmm_dynamic_kernelILi128ELi8ELi4ELi4ELb0",
+                                "spmm_chunk_kernelILi16ELi8ELi2ELi1ELb0", "spmm_dynamic_kernelILi16ELi8ELi2ELi1ELb0"),
                   dry_run=False, log=print, strict=False):
     """Re-schedules the listed kernels inside `lib`. With strict=True (the build) a listed
     kernel that is missing or fails a precondition raises SassSchedError instead of being
@@ -342,7 +350,8 @@ def patch_library(lib, kernels=("spmm_chunk_kernelILi64ELi8ELi4ELi2ELb0", "spmm_
             log(f"{name[:60]}: code not located uniquely (already patched or compressed)")
             failed.append(hit)
             continue
-        edits = plan_patch(code, lambda s: log(f"{name[:60]}: {s}"))
+        edits = plan_patch(code, lambda s: log(f"{name[:60]}: {s}"),
+                           width=64 if any(t in name for t in _NARROW) else 128)
         if not edits:
             failed.append(hit)
             continue

@@ -117,12 +117,12 @@ def test_invalid_column_under_dynamic_dispatch_is_einval(ctx):
     col[nnz // 2] = np.uint32(0x7fffff00)  # far outside X
     vals = rng.random(nnz, np.float32)
     x = rng.random((n, d), np.float32)
-    for dyn in (True, False):
+    for dyn, flags in ((True, 8), (True, 0), (False, 0)):  # 8 = SPMX_CLAIM_KERNEL: spmm_dynamic_kernel
         with pytest.raises(SpmxInvalidArgument, match="column index out of range"):
-            ctx.spmm_host(m, n, rp, col, vals, x, strategy="row", dynamic=dyn)
+            ctx.spmm_host(m, n, rp, col, vals, x, strategy="row", dynamic=dyn, flags=flags)
     # the context is still usable afterwards (no sticky CUDA error)
     col[nnz // 2] = 0
-    y, _ = ctx.spmm_host(m, n, rp, col, vals, x, strategy="row", dynamic=True)
+    y, _ = ctx.spmm_host(m, n, rp, col, vals, x, strategy="row", dynamic=True, flags=8)
     assert np.isfinite(y).all()
 
 

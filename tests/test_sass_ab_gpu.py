@@ -49,7 +49,7 @@ def test_patched_and_as_built_libraries_agree_bitwise(both, name, d_override):
         da = ctx.csr_wrap(a)
         out = []
         for strategy, flags, dyn in (("merge", 0, False), ("row", 0, False), ("merge", EXACT, False),
-                                     ("row", 0, True)):
+                                     ("row", 8, True)):  # 8 = SPMX_CLAIM_KERNEL: the dynamic kernel itself
             p = ctx.plan(da, strategy, 0, dynamic=dyn, flags=flags)
             y = torch.full((a.m, d), float("nan"), device="cuda")
             for _ in range(3):  # repeated launches: a race would not hit the same bits thrice

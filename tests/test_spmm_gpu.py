@@ -15,6 +15,7 @@ from helpers import D_POOL, chain_lengths, north_star_ok, rand_csr, split_row_ma
 pytestmark = pytest.mark.gpu
 
 EXACT = 1
+CLAIM = 8  # SPMX_CLAIM_KERNEL
 LONG_SEG = 128  # interior chunk cuts never split rows shorter than this (snap_len in csrc/spmx_capi.cu)
 STRATS = ("row", "nnz", "merge")
 
@@ -66,8 +67,9 @@ def test_identity_returns_x_bitwise(ctx):
             for fl in (0, EXACT):
                 y, _ = run(ctx, n, n, rp, col, vals, x, s, t, fl)
                 assert np.array_equal(y, x)
-        y, _ = run(ctx, n, n, rp, col, vals, x, "row", t, 0, dynamic=True, batch=16)
-        assert np.array_equal(y, x)
+        for fl in (0, CLAIM):  # dynamic dispatch: served by the work list / by the claim kernel
+            y, _ = run(ctx, n, n, rp, col, vals, x, "row", t, fl, dynamic=True, batch=16)
+            assert np.array_equal(y, x)
 
 
 def test_empty_rows_are_zeroed(ctx):
@@ -118,6 +120,12 @@ def test_reference_golden_instances_default_mode(ctx, golden_instances, oracle):
                 exact_rows = ~split_row_mask(m, cr, cj, g["row_ptr"]) & (lens < LONG_SEG)
                 assert np.array_equal(y[exact_rows].view(np.uint32),
                                       g["y_fused"][exact_rows].view(np.uint32)), (idx, s, t)
+        # dynamic row dispatch in the default mode: the row-split work list, and the literal
+        # claim kernel (row-granular: every row one fmaf chain, bitwise equal to the reference)
+        y, _ = run(ctx, m, n, g["row_ptr"], g["col"], g["vals"], g["x"], "row", 0, 0, dynamic=True, batch=32)
+        assert north_star_ok(y, g["y_unfused"], bound), (idx, "dynamic")
+        y, _ = run(ctx, m, n, g["row_ptr"], g["col"], g["vals"], g["x"], "row", 0, CLAIM, dynamic=True, batch=32)
+        assert np.array_equal(y.view(np.uint32), g["y_fused"].view(np.uint32)), (idx, "claims")
 
 
 def test_executor_checksum_invariant(ctx, oracle):
