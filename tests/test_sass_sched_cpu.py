@@ -14,7 +14,12 @@ import pytest
 from paper_2312_05639_b200 import binding, sass_sched
 
 KERNELS = ("spmm_chunk_kernelILi64ELi8ELi4ELi2ELb0", "spmm_chunk_kernelILi32ELi8ELi4ELi1ELb0",
-           "spmm_chunk_kernelILi128ELi8ELi4ELi4ELb0")
+           "spmm_chunk_kernelILi128ELi8ELi4ELi4ELb0", "spmm_chunk_kernelILi16ELi8ELi2ELi1ELb0")
+
+
+def _width(kernel):
+    """bits per lane of the kernel's row gathers (d = 16: 8 lanes x float2)"""
+    return 64 if any(t in kernel for t in sass_sched._NARROW) else 128
 
 
 @pytest.fixture(scope="module")
@@ -27,7 +32,7 @@ def funcs():
     return sass_sched.disassemble(lib)
 
 
-def _walk_loop(code):
+def _walk_loop(code, gather):
     """(top, end, gathers) of the innermost loop (no backward branch inside) whose body holds
     the most row gathers."""
     best = None
@@ -36,7 +41,7 @@ def _walk_loop(code):
         if not m or int(m.group(1), 16) >= ins.addr:
             continue
         top = next(j for j, c in enumerate(code) if c.addr == int(m.group(1), 16))
-        n = sum(1 for c in code[top:i] if sass_sched._GATHER.search(c.text))
+        n = sum(1 for c in code[top:i] if gather.search(c.text))
         inner = any((mm := re.search(sass_sched._BRA, c.text)) and int(mm.group(1), 16) < c.addr
                     for c in code[top:i])
         if not inner and (best is None or n > best[2]):
@@ -48,10 +53,11 @@ def _walk_loop(code):
 def test_gathers_are_split_over_two_scoreboards(funcs, kernel):
     name = next(n for n in funcs if kernel in n)
     code = funcs[name]
-    top, end, n = _walk_loop(code)
+    gather = sass_sched._GATHERS[_width(kernel)]
+    top, end, n = _walk_loop(code, gather)
     assert n >= 8, "walk loop not found"
     body = code[top:end + 1]
-    loads = [c for c in body if sass_sched._GATHER.search(c.text)]
+    loads = [c for c in body if gather.search(c.text)]
     boards = sorted({c.wb for c in loads})
     assert len(boards) == 2 and 5 in boards, boards
     moved = [c for c in loads if c.wb != 5]
@@ -73,4 +79,4 @@ def test_gathers_are_split_over_two_scoreboards(funcs, kernel):
         else:
             pytest.fail("no wait for the moved gather")
     # a second pass has nothing to do (the gathers are no longer all on SB5)
-    assert sass_sched.plan_patch(code) is None
+    assert sass_sched.plan_patch(code, width=_width(kernel)) is None
