@@ -237,8 +237,8 @@ def roofline_block(name, args, world, m_total, n_cols, nnz_total, d, ms_step, ga
         tbs, probe_ms = gather_peak
         g.update({"l2_to_sm_peak_tbs": tbs * world, "frac": g["achieved_tbs"] / (tbs * world),
                   "peak_source": f"measured in this run right after the timed region (spmx_probe_l2_to_sm: "
-                                 f"random 256-byte rows of an L2-resident 64 MB buffer, LDG.128, 32 warps/SM, "
-                                 f"best of 10, {probe_ms * 1e3:.0f} us per launch)"})
+                                 f"random 256-byte rows of an L2-resident 64 MB buffer, LDG.128, best of 24/32/40/48 "
+                                 f"warps per SM x 10 launches, {probe_ms * 1e3:.0f} us per launch)"})
     roofline["gather"] = g
     if world > 1:
         bytes_repl = bytes_alg + (world - 1) * 4 * n_cols * d  # X is replicated on every rank
@@ -324,7 +324,7 @@ def run_single(args):
         torch.cuda.synchronize()
         window = f"timed region + {extra_steps} identical untimed steps (0.4 s) right after it"
     # the L2 -> SM ceiling at the clocks this run is at (still inside the sampled window)
-    gather_peak = ctx.probe_l2_to_sm(10)
+    gather_peak = ctx.probe_l2_to_sm(10)  # ~15 ms
     clocks = sampler.stop()
     clocks["window"] = window
     gflops = 2.0 * a.nnz * d / (ms_step * 1e-3) / 1e9

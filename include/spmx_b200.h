@@ -184,10 +184,18 @@ int spmx_jit_stats(uint64_t* kernels_compiled, double* seconds);
 /* 1 when the run-time compiler (libnvrtc) can be loaded, i.e. SPMX_JIT_WIDTH can be honoured */
 int spmx_jit_available(void);
 
+/* L2 residency control for the context's stream: kernels launched after this call treat
+ * [base, base + bytes) as a persisting access-policy window (hit ratio hit_ratio, everything else
+ * streaming); bytes == 0 removes the window and resets the persisting lines. The window is clipped
+ * to the device's limits (out_window_bytes, may be NULL). For callers whose hottest X rows are
+ * contiguous (e.g. a column ordering by degree): tools/exp_hot_window.py measures what it buys. */
+int spmx_ctx_l2_window(spmx_ctx* ctx, const void* base, size_t bytes, float hit_ratio,
+                       size_t* out_window_bytes);
+
 /* Measurement aid (bench.py roofline.gather): the L2 -> SM ceiling of this GPU at its current
  * clocks — random 256-byte rows of an L2-resident 64 MB buffer read by 8-lane groups with
- * LDG.128, 32 warps per SM (the SpMM's own access shape at d = 64); best of `repeats` launches,
- * in TB/s over the whole chip, and that launch's duration. Not on the hot path. */
+ * LDG.128 (the SpMM's own access shape at d = 64), at 24, 32, 40 and 48 warps per SM; the best of
+ * `repeats` launches each, in TB/s over the whole chip, and that launch's duration. Not on the hot path. */
 int spmx_probe_l2_to_sm(spmx_ctx* ctx, int repeats, double* out_tbs, double* out_ms);
 
 /* ---- helpers for the reference's report fields ---------------------------------------------- */

@@ -169,6 +169,7 @@ class Lib:
         L.spmx_mg_y_shard.argtypes = [vp, C.c_int, P(vp)]
         L.spmx_mg_download_y.argtypes = [vp, vp]
         L.spmx_mg_download_y_shards.argtypes = [vp, P(vp)]
+        L.spmx_ctx_l2_window.argtypes = [vp, vp, sz, C.c_float, P(sz)]
         L.spmx_probe_l2_to_sm.argtypes = [vp, C.c_int, P(C.c_double), P(C.c_double)]
         L.spmx_mg_allgather_y.argtypes = [vp, fp]
         L.spmx_mg_y_full.argtypes = [vp, C.c_int, P(vp)]
@@ -367,6 +368,14 @@ class Context:
         out = C.c_double()
         self.L.check(self.L.lib.spmx_max_relative_error(self.h, _ptr(y), _ptr(ref), y.numel(),
                                                         C.byref(out)))
+        return out.value
+
+    def l2_window(self, ptr=0, nbytes=0, hit_ratio=1.0) -> int:
+        """Persisting access-policy window on the context's stream (nbytes=0 clears it).
+        Returns the window size actually set."""
+        out = C.c_size_t()
+        self.L.check(self.L.lib.spmx_ctx_l2_window(self.h, C.c_void_p(ptr or None), nbytes, hit_ratio,
+                                                   C.byref(out)))
         return out.value
 
     def probe_l2_to_sm(self, repeats=10):

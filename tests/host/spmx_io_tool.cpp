@@ -7,11 +7,13 @@
 //   spmx_io_tool mtx-to-jspm <in.mtx> <out.jspm>
 //   spmx_io_tool copy-jspm <in.jspm> <out.jspm>
 //   spmx_io_tool validate <in.jspm|in.mtx>
+//   spmx_io_tool config <c1..c5> <scale|0> <rows|0> <out.jspm> <out_x.f32>   (host/spmx_workloads.hpp)
 #include <cstdio>
 #include <cstring>
 #include <string>
 
 #include "../../paper_2312_05639_b200/host/spmx_io.hpp"
+#include "../../paper_2312_05639_b200/host/spmx_workloads.hpp"
 
 static bool ends_with(const std::string& s, const char* suf) {
   const size_t n = std::strlen(suf);
@@ -37,6 +39,13 @@ int main(int argc, char** argv) {
       spmx::save_csr_cache(spmx::load_matrix_market(argv[2]), argv[3]);
     } else if (cmd == "copy-jspm" && argc == 4) {
       spmx::save_csr_cache(spmx::load_csr_cache(argv[2]), argv[3]);
+    } else if (cmd == "config" && argc == 7) {
+      spmx::workloads::Config c = spmx::workloads::make_config(argv[2], std::atoi(argv[3]), std::atoll(argv[4]));
+      spmx::save_csr_cache(c.a, argv[5]);
+      FILE* f = std::fopen(argv[6], "wb");
+      if (!f) throw std::runtime_error("cannot open for write");
+      std::fwrite(c.x.data.data(), 4, c.x.data.size(), f);
+      std::fclose(f);
     } else if (cmd == "validate" && argc == 3) {
       const spmx::CsrMatrix a = ends_with(argv[2], ".jspm") ? spmx::load_csr_cache(argv[2])
                                                             : spmx::load_matrix_market(argv[2]);

@@ -82,3 +82,22 @@ def test_csv_sweep_files_and_exit_codes(cli, tmp_path):
     # dynamic dispatch is silently limited to the row strategy, as in the reference (bench.cpp:155)
     r = run(cli, "--synthetic", 500, "--strategy", "nnz", "--dispatch", "dynamic")
     assert r.returncode == 0 and json.loads(r.stdout)["strategy"] == "nnz"
+
+
+def test_baseline_configs_from_the_cli(cli, oracle):
+    """--config cN: the CLI generates BASELINE.json's configurations itself (host C++ generators,
+    host/spmx_workloads.hpp) — the same arrays as workloads.py, so the exact-order y_checksum
+    equals the oracle's on the Python-generated sibling, also through the multi-GPU driver."""
+    from paper_2312_05639_b200 import workloads as W
+    for name, scale in (("c2", 12), ("c5", 11)):
+        a, x, spec = W.make_config(name, scale_override=scale)
+        rp, col, vals = a.numpy()
+        want = oracle.checksum(oracle.spmm_fused(a.m, a.n, rp, col, vals, x.numpy()))
+        for extra in ((), ("--gpus", 1, "--shards", 3)):
+            r = run(cli, "--config", name, "--scale", scale, "--strategy", "merge", "--dispatch", "static",
+                    "--backend", "interp", "--verify", *extra)
+            assert r.returncode == 0, r.stderr
+            j = json.loads(r.stdout)
+            assert (j["m"], j["nnz"], j["d"]) == (a.m, a.nnz, spec["d"])
+            assert j["y_checksum"] == want and j["max_rel_err"] <= 1e-5
+    assert run(cli, "--config", "c9").returncode == 1

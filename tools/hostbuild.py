@@ -16,7 +16,8 @@ IO_TOOL_SRC = os.path.join(_ROOT, "tests", "host", "spmx_io_tool.cpp")
 IO_TOOL = os.path.join(_ROOT, "tests", "host", "spmx_io_tool")
 CLI_SRC = os.path.join(_ROOT, "tools", "spmx_bench_b200.cpp")
 CLI = os.path.join(_PKG, "spmx_bench_b200")
-_HOST_HDRS = [os.path.join(_PKG, "host", h) for h in ("spmx_b200.hpp", "spmx_io.hpp", "spmx_types.hpp")]
+_HOST_HDRS = [os.path.join(_PKG, "host", h) for h in ("spmx_b200.hpp", "spmx_io.hpp", "spmx_types.hpp",
+                                                        "spmx_workloads.hpp")]
 
 
 def _stale(target, deps):
@@ -26,7 +27,7 @@ def _stale(target, deps):
 def build_io_tool(verbose: bool = False) -> str:
     """Host-only tool over host/spmx_io.hpp (no CUDA): used by the CPU test-suite."""
     if _stale(IO_TOOL, [IO_TOOL_SRC] + _HOST_HDRS):
-        cmd = ["g++", "-std=c++20", "-O2", "-Wall", "-o", IO_TOOL, IO_TOOL_SRC]
+        cmd = ["g++", "-std=c++20", "-O2", "-Wall", "-fopenmp", "-o", IO_TOOL, IO_TOOL_SRC]
         if verbose:
             print(" ".join(cmd), file=sys.stderr)
         subprocess.check_call(cmd)
@@ -36,7 +37,7 @@ def build_io_tool(verbose: bool = False) -> str:
 def build_cli(verbose: bool = False) -> str:
     """spmx_bench_b200: the reference's bench CLI for the B200 path (tools/spmx_bench_b200.cpp)."""
     if _stale(CLI, [CLI_SRC, os.path.join(_ROOT, "include", "spmx_b200.h")] + _HOST_HDRS):
-        cmd = ["g++", "-std=c++20", "-O2", "-Wall", "-o", CLI, CLI_SRC, "-L" + _PKG, "-lspmx_b200",
+        cmd = ["g++", "-std=c++20", "-O2", "-Wall", "-fopenmp", "-o", CLI, CLI_SRC, "-L" + _PKG, "-lspmx_b200",
                "-Wl,-rpath,$ORIGIN", "-L/usr/local/cuda/lib64", "-lcudart"]
         if verbose:
             print(" ".join(cmd), file=sys.stderr)

@@ -3,7 +3,9 @@
 // (0 ok, 1 usage/runtime error, 2 verification failure), plus the GPU-side fields
 // bytes_algorithmic, gbs, roofline_frac, n_chunks, gpus. SURVEY.md §8 row f1.
 //
-//   spmx_bench_b200 [--matrix f.mtx|f.jspm | --synthetic ROWS [--avg-nnz A] [--skew S]]
+//   spmx_bench_b200 [--matrix f.mtx|f.jspm | --synthetic ROWS [--avg-nnz A] [--skew S]
+//                    | --config c1..c5 [--scale S | --rows R]]   (BASELINE.json's configurations,
+//                                                                 host/spmx_workloads.hpp; X and d come with them)
 //                   [--cols D] [--strategy row|nnz|merge] [--dispatch static|dynamic]
 //                   [--backend native|interp] [--threads T] [--batch-size B] [--trials K]
 //                   [--seed S] [--verify] [--no-jit] [--format json|csv] [--report FILE]
@@ -26,6 +28,7 @@
 
 #include "../paper_2312_05639_b200/host/spmx_b200.hpp"
 #include "../paper_2312_05639_b200/host/spmx_io.hpp"
+#include "../paper_2312_05639_b200/host/spmx_workloads.hpp"
 
 using namespace spmx;
 
@@ -38,6 +41,10 @@ struct Cli {
   int64_t synthetic_rows = 0;
   double avg_nnz = 16.0, skew = 0.0;
   int cols = 16;
+  bool cols_given = false;
+  std::string config;  // BASELINE.json configuration c1 .. c5
+  int scale = 0;
+  int64_t rows = 0;
   std::string strategy = "row", dispatch = "dynamic", backend = "native";
   unsigned threads = 0, trials = 1;
   uint64_t batch_size = 128, seed = 42;
@@ -133,7 +140,16 @@ RunConfig make_run_config(const Cli& c) {
   return cfg;
 }
 
+workloads::Dist config_x_dist(const std::string& config) {
+  return config == "c3" ? workloads::Dist::Normal : workloads::Dist::UniformPm1;
+}
+
 CsrMatrix load_input(const Cli& c, std::string& name) {
+  if (!c.config.empty()) {
+    name = c.config + (c.scale ? "@scale" + std::to_string(c.scale) : "") +
+           (c.rows ? "@rows" + std::to_string(c.rows) : "");
+    return workloads::make_config(c.config, c.scale, c.rows).a;
+  }
   if (!c.matrix_path.empty()) {
     name = c.matrix_path;
     const std::string& p = c.matrix_path;
@@ -195,7 +211,9 @@ void write_report(const Cli& c, const std::string& text) {
   out << text;
 }
 
-DenseMatrix dense_operand(const CsrMatrix& a, int d, uint64_t seed) {
+DenseMatrix dense_operand(const Cli& c, const CsrMatrix& a, int d, uint64_t seed) {
+  if (!c.config.empty())  // the configuration's own X (its seed and distribution), d columns
+    return workloads::dense(a.n, d, workloads::make_config_seed(c.config), config_x_dist(c.config));
   DenseMatrix x = random_dense(a.n > 0 ? a.n : 1, d, seed);
   if (a.n == 0) x.rows = 0;
   return x;
@@ -205,10 +223,11 @@ int run_single(const Cli& c) {
   std::string name;
   CsrMatrix a = load_input(c, name);
   if (!c.save_cache_path.empty()) save_csr_cache(a, c.save_cache_path);
-  const DenseMatrix x = dense_operand(a, c.cols, c.seed);
+  const int cols = (!c.config.empty() && !c.cols_given) ? workloads::config_width(c.config) : c.cols;
+  const DenseMatrix x = dense_operand(c, a, cols, c.seed);
   const RunConfig cfg = make_run_config(c);
   auto [y, rep] = run_spmm(a, x, cfg);
-  const Row r = report_row(name, a, c.cols, cfg, rep, checksum(y), c.peak_gbs);
+  const Row r = report_row(name, a, cols, cfg, rep, checksum(y), c.peak_gbs);
   write_report(c, c.format == "csv" ? csv_header() + csv_row(r) : r.json(0) + "\n");
   if (rep.max_rel_err && *rep.max_rel_err > kVerifyTolerance) {
     std::cerr << "verification FAILED: max_rel_err = " << *rep.max_rel_err << "\n";
@@ -229,7 +248,7 @@ int run_sweep(const Cli& c) {
         cell.strategy = strat; cell.cols = d; cell.backend = backend;
         try {
           const RunConfig cfg = make_run_config(cell);
-          const DenseMatrix x = dense_operand(a, d, c.seed);
+          const DenseMatrix x = dense_operand(c, a, d, c.seed);
           auto [y, rep] = run_spmm(a, x, cfg);
           Row r = report_row(name, a, d, cfg, rep, checksum(y), c.peak_gbs);
           r.str("status", "ok");
@@ -303,7 +322,10 @@ Cli parse(int argc, char** argv) {
     else if (key == "--gpus") c.gpus = unsigned(positive(value()));
     else if (key == "--shards") c.shards = unsigned(positive(value()));
     else if (key == "--shard-by") c.shard_by = value();
-    else if (!c.sweep && key == "--cols") c.cols = int(positive(value()));
+    else if (!c.sweep && key == "--cols") { c.cols = int(positive(value())); c.cols_given = true; }
+    else if (key == "--config") c.config = value();
+    else if (key == "--scale") c.scale = int(positive(value()));
+    else if (key == "--rows") c.rows = positive(value());
     else if (!c.sweep && key == "--strategy") c.strategy = value();
     else if (!c.sweep && key == "--backend") c.backend = value();
     else if (!c.sweep && key == "--save-cache") c.save_cache_path = value();
