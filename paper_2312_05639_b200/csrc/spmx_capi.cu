@@ -8,6 +8,7 @@
 
 #include <cuda_runtime.h>
 
+#include <algorithm>
 #include <atomic>
 #include <chrono>
 #include <cstdio>
@@ -89,6 +90,8 @@ inline u64 chunk_items_for(u64 items, int sm_count) {
 // interior chunk boundaries never cut a row shorter than this
 inline u64 snap_len() { return env_u64("SPMX_SNAP_LEN", 128); }
 inline u64 default_parts_per_sm() { return env_u64("SPMX_PARTS_PER_SM", 8); }
+// exact-order plans: rows at least this long run in spmm_long_row_kernel (0 disables)
+inline u64 long_row_min() { return env_u64("SPMX_LONG_ROW", 1024); }
 
 inline unsigned blocks_for(u64 n, unsigned threads = 256) {
   return (unsigned)((n + threads - 1) / threads);
@@ -105,6 +108,8 @@ struct spmx_ctx {
   cudaEvent_t ev0 = nullptr, ev1 = nullptr;
   int* d_err = nullptr;  // device-side error flag for validation
   cudaStream_t s_compute = nullptr, s_d2h = nullptr, s_x = nullptr;  // spmx_spmm_host pipeline (lazy)
+  cudaStream_t s_aux = nullptr;  // long rows of exact-order plans run beside the main kernel (lazy)
+  cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
   std::vector<cudaEvent_t> pipe_events;                // created once, reused by every call
   // grow-only staging used by spmx_spmm_host
   void* ws[5] = {nullptr, nullptr, nullptr, nullptr, nullptr};
@@ -144,6 +149,8 @@ struct spmx_plan {
   uint32_t* short_buf = nullptr;    // [count | boundaries closing the other chains]
   uint32_t* short_list = nullptr;   // = short_buf + 1
   uint32_t n_short = 0;
+  spmx_dev::LongRow* long_rows = nullptr;  // exact-order plans: rows run by spmm_long_row_kernel
+  uint32_t n_long_rows = 0;
   u64* counter = nullptr;    // dynamic dispatch
   bool may_carry = false;
   mutable float* carry = nullptr;  // n_chunks x ld floats, grown on demand
@@ -394,6 +401,48 @@ void launch_fixup(const spmx_plan* p, u64 tb, u64 te, float* d_y, int ldx, int c
   post_launch();
 }
 
+// spmm_long_row_kernel for the plan's long rows (exact-order plans), columns [c0, c0 + dw) of X
+// and Y, on the context's auxiliary stream beside the main kernel: forked from `st` here, joined
+// by the caller's join_long_rows after the main kernel has been queued.
+template <int C, int PIECE>
+void launch_long_one(const spmx_plan* p, const spmx_dev::SpmmArgs& args, cudaStream_t st) {
+  const size_t smem = spmx_dev::long_row_smem_bytes(args.dw, PIECE);
+  static std::atomic<uint64_t> done_mask{0};  // one bit per device
+  int dev = 0;
+  CUDA_CHECK(cudaGetDevice(&dev));
+  if (!(done_mask.load() >> (dev & 63) & 1)) {
+    done_mask.fetch_or(1ull << (dev & 63));
+    // the narrowest slab has the most positions per tile, i.e. the largest column/value rings
+    CUDA_CHECK(cudaFuncSetAttribute(spmx_dev::spmm_long_row_kernel<C, PIECE>,
+                                    cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                    (int)spmx_dev::long_row_smem_bytes(1, PIECE)));
+  }
+  spmx_dev::spmm_long_row_kernel<C, PIECE>
+      <<<p->n_long_rows, spmx_dev::kLongThreads, smem, st>>>(args, p->long_rows);
+  post_launch();
+}
+
+void launch_long_rows(spmx_ctx* ctx, const spmx_plan* p, spmx_dev::SpmmArgs args, int c0, int dw, bool piece4,
+                      cudaStream_t st) {
+  if (!ctx->s_aux) {
+    CUDA_CHECK(cudaStreamCreateWithFlags(&ctx->s_aux, cudaStreamNonBlocking));
+    CUDA_CHECK(cudaEventCreateWithFlags(&ctx->ev_fork, cudaEventDisableTiming));
+    CUDA_CHECK(cudaEventCreateWithFlags(&ctx->ev_join, cudaEventDisableTiming));
+  }
+  CUDA_CHECK(cudaEventRecord(ctx->ev_fork, st));
+  CUDA_CHECK(cudaStreamWaitEvent(ctx->s_aux, ctx->ev_fork, 0));
+  for (int cc = c0; cc < c0 + dw; cc += 128) {  // the ring holds slabs of up to 128 columns
+    args.c0 = cc;
+    args.dw = std::min(128, c0 + dw - cc);
+    const int cols_per_lane = (args.dw + 31) / 32;
+    const bool p4 = piece4 && args.dw % 4 == 0 && cc % 4 == 0;
+    if (cols_per_lane <= 1) p4 ? launch_long_one<1, 4>(p, args, ctx->s_aux) : launch_long_one<1, 1>(p, args, ctx->s_aux);
+    else if (cols_per_lane == 2) p4 ? launch_long_one<2, 4>(p, args, ctx->s_aux) : launch_long_one<2, 1>(p, args, ctx->s_aux);
+    else p4 ? launch_long_one<4, 4>(p, args, ctx->s_aux) : launch_long_one<4, 1>(p, args, ctx->s_aux);
+  }
+  CUDA_CHECK(cudaEventRecord(ctx->ev_join, ctx->s_aux));
+}
+
 // Launches the SpMM (and carry fix-up) for chunks [cb, ce) of the plan's work list on `st`.
 // The fix-up handles the chains that start in a chunk in [first_lo, first_hi); with
 // fixup_only the SpMM itself is not launched (the host pipeline's deferred chains).
@@ -435,6 +484,10 @@ void run_kernels(spmx_ctx* ctx, const spmx_plan* p, const spmx_csr* a, const flo
   args.counter = p->counter;
   args.batch = p->batch;
 
+  // exact-order plans: the long rows, beside the main kernel (the plan took them out of its list)
+  const bool long_rows = p->n_long_rows > 0 && !fixup_only && !p->claims;
+  if (long_rows) launch_long_rows(ctx, p, args, 0, (int)d, vec_max == 4, st);
+
   // run-time instantiation for exactly this d (SPMX_JIT_WIDTH): one launch covers the whole
   // width when it fits 32 lanes x 8 tiles; the precompiled widths and dynamic plans keep
   // their own kernels
@@ -458,6 +511,7 @@ void run_kernels(spmx_ctx* ctx, const spmx_plan* p, const spmx_csr* a, const flo
     if (p->may_carry && te > tb) {
       launch_fixup(p, tb, te, d_y, (int)d, 0, (int)d, st, first_lo, first_hi);
     }
+    if (long_rows) CUDA_CHECK(cudaStreamWaitEvent(st, ctx->ev_join, 0));
     return;
   }
 
@@ -506,6 +560,7 @@ void run_kernels(spmx_ctx* ctx, const spmx_plan* p, const spmx_csr* a, const flo
       launch_fixup(p, tb, te, d_y, (int)d, (int)c0, dw, st, first_lo, first_hi);
     }
   }
+  if (long_rows) CUDA_CHECK(cudaStreamWaitEvent(st, ctx->ev_join, 0));
 }
 
 void plan_free(spmx_plan* p) {
@@ -518,6 +573,7 @@ void plan_free(spmx_plan* p) {
   dev_free_async(p->ctx, p->short_buf);
   dev_free_async(p->ctx, p->chunk_nnz);
   dev_free_async(p->ctx, p->counter);
+  dev_free_async(p->ctx, p->long_rows);
   dev_free_async(p->ctx, p->carry);
   p->magic = 0;
   delete p;
@@ -587,8 +643,49 @@ spmx_plan* plan_build(spmx_ctx* ctx, const spmx_csr* a, int strategy, unsigned p
     // 3. work list: exact -> one chunk per range, boundaries on rows; otherwise ranges heavier
     //    than the chunk budget are cut along the merge path (interior cuts snapped to the start
     //    of short rows)
+    u64 long_min = 0;
     if (exact) {
+      // Long rows get work-list boundaries of their own (before and after the row), so that each
+      // is a chunk by itself: the list of such rows is small, it is sorted and merged with the
+      // strategy's boundaries on the host.
       p->n_chunks = parts;
+      long_min = long_row_min();
+      if (long_min && nnz >= long_min) {
+        const size_t cap = (size_t)(nnz / long_min) + 1;
+        u64* d_list = tmp.get<u64>(cap);
+        unsigned* d_n = tmp.get<unsigned>(1);
+        CUDA_CHECK(cudaMemsetAsync(d_n, 0, sizeof(unsigned), ctx->stream));
+        spmx_dev::long_rows_kernel<<<validate_grid(ctx, m), 256, 0, ctx->stream>>>(a->row_ptr, m, long_min,
+                                                                                    d_list, d_n);
+        post_launch();
+        unsigned n_long = 0;
+        CUDA_CHECK(cudaMemcpyAsync(&n_long, d_n, sizeof(unsigned), cudaMemcpyDeviceToHost, ctx->stream));
+        CUDA_CHECK(cudaStreamSynchronize(ctx->stream));
+        if (n_long > 0) {
+          std::vector<u64> rows(n_long), bnd((size_t)parts + 1);
+          CUDA_CHECK(cudaMemcpyAsync(rows.data(), d_list, (size_t)n_long * 8, cudaMemcpyDeviceToHost, ctx->stream));
+          CUDA_CHECK(cudaMemcpyAsync(bnd.data(), d_bnd, ((size_t)parts + 1) * 8, cudaMemcpyDeviceToHost, ctx->stream));
+          CUDA_CHECK(cudaStreamSynchronize(ctx->stream));
+          bnd.reserve(bnd.size() + 2 * (size_t)n_long);
+          for (u64 r : rows) { bnd.push_back(r); bnd.push_back(r + 1); }
+          std::sort(bnd.begin(), bnd.end());
+          bnd.erase(std::unique(bnd.begin(), bnd.end()), bnd.end());
+          p->n_chunks = bnd.size() - 1;
+          u64* d_bnd2 = tmp.get<u64>(bnd.size());
+          d_diag = tmp.get<u64>(bnd.size());
+          CUDA_CHECK(cudaMemcpyAsync(d_bnd2, bnd.data(), bnd.size() * 8, cudaMemcpyHostToDevice, ctx->stream));
+          spmx_dev::boundaries_to_diagonals_kernel<<<blocks_for(bnd.size()), 256, 0, ctx->stream>>>(
+              a->row_ptr, d_bnd2, bnd.size(), d_diag);
+          post_launch();
+          CUDA_CHECK(cudaStreamSynchronize(ctx->stream));  // bnd goes out of scope
+          p->long_rows = dev_alloc_async<spmx_dev::LongRow>(ctx, (size_t)n_long);
+        } else {
+          long_min = 0;
+        }
+      } else {
+        long_min = 0;
+      }
+      if (p->n_chunks >= 0xffffffffull) throw InvalidArg("plan: work list too long");
       p->chunk_row = dev_alloc_async<u64>(ctx, (size_t)p->n_chunks + 1);
       p->chunk_nnz = dev_alloc_async<u64>(ctx, (size_t)p->n_chunks + 1);
       spmx_dev::merge_search_kernel<<<blocks_for(p->n_chunks + 1), 256, 0, ctx->stream>>>(
@@ -645,10 +742,29 @@ spmx_plan* plan_build(spmx_ctx* ctx, const spmx_csr* a, int strategy, unsigned p
     }
     if (p->n_chunks > 0) {
       p->work = dev_alloc_async<spmx_dev::WorkItem>(ctx, (size_t)p->n_chunks);
-      spmx_dev::work_items_kernel<spmx_dev::WorkItem>
+      unsigned* d_nlong = tmp.get<unsigned>(1);
+      CUDA_CHECK(cudaMemsetAsync(d_nlong, 0, sizeof(unsigned), ctx->stream));
+      spmx_dev::work_items_kernel<spmx_dev::WorkItem, spmx_dev::LongRow>
           <<<blocks_for(p->n_chunks, spmx_dev::kSortTile), spmx_dev::kSortTile, 0, ctx->stream>>>(
-              p->chunk_row, p->chunk_nnz, p->n_chunks, p->work);
+              p->chunk_row, p->chunk_nnz, p->n_chunks, p->work, p->long_rows ? long_min : 0, p->long_rows,
+              d_nlong);
       post_launch();
+      CUDA_CHECK(cudaMemcpyAsync(&p->n_long_rows, d_nlong, sizeof(unsigned), cudaMemcpyDeviceToHost,
+                                 ctx->stream));
+      if (p->long_rows) {  // longest rows first: a row is one CTA's serial chain, the tail is the longest
+        CUDA_CHECK(cudaStreamSynchronize(ctx->stream));
+        std::vector<spmx_dev::LongRow> lr(p->n_long_rows);
+        CUDA_CHECK(cudaMemcpyAsync(lr.data(), p->long_rows, lr.size() * sizeof(spmx_dev::LongRow),
+                                   cudaMemcpyDeviceToHost, ctx->stream));
+        CUDA_CHECK(cudaStreamSynchronize(ctx->stream));
+        std::sort(lr.begin(), lr.end(), [](const spmx_dev::LongRow& x, const spmx_dev::LongRow& y) {
+          const u64 lx = x.j1 - x.j0, ly = y.j1 - y.j0;
+          return lx != ly ? lx > ly : x.row < y.row;
+        });
+        CUDA_CHECK(cudaMemcpyAsync(p->long_rows, lr.data(), lr.size() * sizeof(spmx_dev::LongRow),
+                                   cudaMemcpyHostToDevice, ctx->stream));
+        CUDA_CHECK(cudaStreamSynchronize(ctx->stream));
+      }
     }
     // a work item's nonzero offsets are 32-bit inside the kernel: every chunk must span fewer
     // than 2^32 nonzeros (only exact-order plans, one chunk per strategy range, can exceed it)
@@ -734,6 +850,9 @@ int spmx_ctx_destroy(spmx_ctx* ctx) {
     if (ctx->s_compute) cudaStreamDestroy(ctx->s_compute);
     if (ctx->s_d2h) cudaStreamDestroy(ctx->s_d2h);
     if (ctx->s_x) cudaStreamDestroy(ctx->s_x);
+    if (ctx->s_aux) cudaStreamDestroy(ctx->s_aux);
+    if (ctx->ev_fork) cudaEventDestroy(ctx->ev_fork);
+    if (ctx->ev_join) cudaEventDestroy(ctx->ev_join);
     cudaEventDestroy(ctx->ev0);
     cudaEventDestroy(ctx->ev1);
     if (ctx->own_stream) cudaStreamDestroy(ctx->stream);
@@ -1136,7 +1255,8 @@ int spmx_spmm_host(spmx_ctx* ctx, int64_t m, int64_t n, int64_t nnz, const uint6
       // blocks = runs of whole chunks with about equal nonzero counts
       int nblocks = 1;
       std::vector<u64> cb{0, plan->n_chunks}, row_b{0, (u64)m}, nnz_b{0, (u64)nnz};
-      if (!plan->claims && plan->n_chunks >= 64 && nnz > (1 << 20)) {
+      // (long rows of an exact-order plan read nonzeros of every block: no block pipeline then)
+      if (!plan->claims && plan->n_long_rows == 0 && plan->n_chunks >= 64 && nnz > (1 << 20)) {
         nblocks = (int)std::min<u64>(kMaxBlocks, std::max<u64>(2, env_u64("SPMX_HOST_BLOCKS", 8)));
         cb.assign(nblocks + 1, 0);
         row_b.assign(nblocks + 1, 0);

@@ -204,16 +204,26 @@ __global__ void chunk_coords_kernel(const u64* __restrict__ row_ptr, u64 m, u64 
 #endif
 constexpr int kSortTile = SPMX_SORT_TILE;
 
-template <typename Item>
+// long_min > 0 (exact-order plans): a chunk that is exactly one row of long_min nonzeros or more
+// is taken out of this list (its work item becomes an empty piece) and appended to long_rows,
+// the work list of spmm_long_row_kernel.
+template <typename Item, typename Long>
 __global__ void __launch_bounds__(kSortTile)
 work_items_kernel(const u64* __restrict__ chunk_row, const u64* __restrict__ chunk_nnz,
-                  u64 n_chunks, Item* __restrict__ work) {
+                  u64 n_chunks, Item* __restrict__ work, u64 long_min, Long* __restrict__ long_rows,
+                  unsigned* __restrict__ long_count) {
   __shared__ u64 key[kSortTile];
   const u64 base = (u64)blockIdx.x * kSortTile;
   const u64 c = base + threadIdx.x;
   u64 k = ~0ull;  // padding sorts last
   if (c < n_chunks) {
-    const u64 span = chunk_nnz[c + 1] - chunk_nnz[c];
+    u64 span = chunk_nnz[c + 1] - chunk_nnz[c];
+    if (long_min && span >= long_min && chunk_row[c + 1] == chunk_row[c] + 1) {
+      Long lr;
+      lr.row = chunk_row[c]; lr.j0 = chunk_nnz[c]; lr.j1 = chunk_nnz[c + 1];
+      long_rows[atomicAdd(long_count, 1u)] = lr;
+      span = 0;
+    }
     k = (min(span, 0xffffffffull) << 32) | threadIdx.x;
   }
   key[threadIdx.x] = k;
@@ -235,10 +245,20 @@ work_items_kernel(const u64* __restrict__ chunk_row, const u64* __restrict__ chu
     Item it;
     it.r0 = chunk_row[src]; it.j0 = chunk_nnz[src];
     it.r1 = chunk_row[src + 1]; it.j1 = chunk_nnz[src + 1];
+    if ((key[threadIdx.x] >> 32) == 0 && it.j1 != it.j0) { it.r1 = it.r0; it.j1 = it.j0; }  // a long row: not ours
     it.chunk = src;
     it.pad_ = 0;
     work[slot] = it;
   }
+}
+
+// Rows of long_min nonzeros or more, in no particular order (exact-order plans: these rows get
+// work-list boundaries of their own and run in spmm_long_row_kernel).
+__global__ void long_rows_kernel(const u64* __restrict__ row_ptr, u64 m, u64 long_min,
+                                 u64* __restrict__ list, unsigned* __restrict__ count) {
+  const u64 stride = (u64)gridDim.x * blockDim.x;
+  for (u64 r = (u64)blockIdx.x * blockDim.x + threadIdx.x; r < m; r += stride)
+    if (__ldg(row_ptr + r + 1) - __ldg(row_ptr + r) >= long_min) list[atomicAdd(count, 1u)] = r;
 }
 
 // Largest nonzero span of a chunk (the kernel keeps nonzero offsets inside a chunk in 32 bits).

@@ -144,3 +144,43 @@ def test_structure_only_handle(ctx, oracle):
         ctx.spmm(p, s, torch.zeros(1, 4, device="cuda"), torch.zeros(m, 4, device="cuda"))
     p.close()
     s.close()
+
+
+@pytest.mark.parametrize("d", [64, 32, 128, 100, 45, 7, 300])
+def test_long_rows_in_exact_order_mode_are_bitwise(ctx, oracle, d):
+    """Exact-order plans hand rows of 1024 nonzeros or more to spmm_long_row_kernel (one CTA per
+    row: all threads gather, one warp runs the fmaf chain in CSR order). Bitwise equal to the
+    oracle's fused result (interp.cpp:36-51) for every strategy, for widths that are not a
+    multiple of 4 or 32, wider than one 128-column slab, and for X / Y that are only 4-byte
+    aligned (scalar loads); rows just below and at the threshold included."""
+    from paper_2312_05639_b200.binding import EXACT_ORDER
+    rng = np.random.default_rng(21)
+    lens = [5000, 0, 1023, 1024, 3, 70_000, 0, 0, 1500, 17] + [int(v) for v in rng.integers(0, 40, size=300)]
+    m, n = len(lens), 3000
+    rp = np.zeros(m + 1, np.uint64)
+    rp[1:] = np.cumsum(np.asarray(lens, np.uint64))
+    nnz = int(rp[-1])
+    col = rng.integers(0, n, size=nnz, dtype=np.int64).astype(np.uint32)
+    vals = (rng.random(nnz, np.float32) * 2 - 1).astype(np.float32)
+    x = (rng.random((n, d), np.float32) * 2 - 1).astype(np.float32)
+    want = oracle.spmm_fused(m, n, rp, col, vals, x)
+    a = ctx.csr_upload(m, n, rp, col, vals)
+    for shift in (0, 1):  # 1: X and Y start 4 bytes off a 16-byte boundary
+        xbuf = torch.zeros(n * d + 4, device="cuda")
+        ybuf = torch.full((m * d + 4,), float("nan"), device="cuda")
+        xd = xbuf[shift:shift + n * d].view(n, d)
+        yd = ybuf[shift:shift + m * d].view(m, d)
+        xd.copy_(torch.from_numpy(x))
+        for strat in ("row", "nnz", "merge"):
+            for parts in (0, 3):
+                p = ctx.plan(a, strat, parts, flags=EXACT_ORDER)
+                yd.fill_(float("nan"))
+                ctx.spmm(p, a, xd, yd)
+                ctx.synchronize()
+                got = yd.cpu().numpy()
+                assert np.array_equal(got.view(np.uint32), want.view(np.uint32)), (d, shift, strat, parts)
+                p.close()
+    # the host-buffer entry point takes the same route (one block when the plan has long rows)
+    yh, _ = ctx.spmm_host(m, n, rp, col, vals, x, strategy="merge", flags=EXACT_ORDER)
+    assert np.array_equal(yh.view(np.uint32), want.view(np.uint32))
+    a.close()
