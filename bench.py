@@ -282,16 +282,22 @@ def run_single(args):
     vals_n, x_n, y_n = vals_h.numpy(), x_h.numpy(), y_h.numpy()
 
     # ---- CPU baseline first (nothing of ours is running on the host or the GPU meanwhile) ----
-    # On ordinary (pageable) copies of the arrays, as the reference arm has them: page-locked
-    # memory is not backed by transparent huge pages and the CPU's random X-row gathers ran
-    # 1.8x slower on it (61 vs 113 GFLOP/s on c2).
+    # It IS the reference arm, run as a child process (python bench.py --impl reference): the same
+    # code, arrays and process conditions the driver's own reference run has, so the two numbers
+    # agree by construction (measured inside this process, after CUDA start-up and host-buffer
+    # pinning, the same run_spmm call took 31 ms instead of 18 ms on c2).
     cpu = None
     if not args.no_cpu_baseline:
-        trials = 5 if a.nnz < 80_000_000 else 3
-        times, kind, cores, mode = cpu_reference_run(np.array(rp_n), np.array(col_n), np.array(vals_n),
-                                                     np.array(x_n), a.m, a.n, args.strategy,
-                                                     trials=trials, warm=2)
-        cpu = cpu_block(times, kind, cores, mode, a.nnz, d, f"full {name} workload (pageable host arrays)")
+        cmd = [sys.executable, os.path.abspath(__file__), "--impl", "reference", "--workload", name,
+               "--strategy", args.strategy, "--steps", "5" if a.nnz < 80_000_000 else "3", "--warmup", "2"]
+        if args.scale is not None:
+            cmd += ["--scale", str(args.scale)]
+        env = {k: v for k, v in os.environ.items() if k not in ("RANK", "WORLD_SIZE", "LOCAL_RANK")}
+        try:
+            out = subprocess.run(cmd, capture_output=True, text=True, timeout=900, env=env).stdout
+            cpu = json.loads([l for l in out.splitlines() if l.startswith("{")][-1])["cpu_baseline"]
+        except Exception as e:  # the GPU numbers do not depend on it
+            cpu = {"value": None, "unit": UNIT, "error": f"reference arm child failed: {e!r}"}
 
     torch.cuda.empty_cache()  # hand the generator's scratch back: the library allocates with cudaMalloc
     da = ctx.csr_wrap(a)

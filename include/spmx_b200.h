@@ -65,10 +65,10 @@ extern "C" {
 
 #define SPMX_CLAIM_KERNEL 8u /* dynamic plans only: run the literal form of the reference's dynamic
                                dispatch (persistent warps claim `batch` rows at a time from a device
-                               counter, rows never cut) in the default mode too. Exact-order dynamic
-                               plans always do. Without it a default-mode dynamic plan is served by
-                               the row-split work list, whose chunks the hardware hands to the SMs
-                               as they free up (and whose long rows are shared between chunks). */
+                               counter, rows never cut). Without it a dynamic plan is served by the
+                               row-split work list, whose chunks the hardware hands to the SMs as
+                               they free up (long rows shared between chunks in the default mode,
+                               given to the long-row kernel in exact-order mode). Same result. */
 
 typedef struct spmx_ctx spmx_ctx;   /* one per (device, stream) */
 typedef struct spmx_csr spmx_csr;   /* A resident on the device */

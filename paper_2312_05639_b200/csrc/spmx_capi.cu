@@ -404,7 +404,7 @@ void launch_fixup(const spmx_plan* p, u64 tb, u64 te, float* d_y, int ldx, int c
 // spmm_long_row_kernel for the plan's long rows (exact-order plans), columns [c0, c0 + dw) of X
 // and Y, on the context's auxiliary stream beside the main kernel: forked from `st` here, joined
 // by the caller's join_long_rows after the main kernel has been queued.
-template <int C, int PIECE>
+template <int PIECE>
 void launch_long_one(const spmx_plan* p, const spmx_dev::SpmmArgs& args, cudaStream_t st) {
   const size_t smem = spmx_dev::long_row_smem_bytes(args.dw, PIECE);
   static std::atomic<uint64_t> done_mask{0};  // one bit per device
@@ -413,11 +413,11 @@ void launch_long_one(const spmx_plan* p, const spmx_dev::SpmmArgs& args, cudaStr
   if (!(done_mask.load() >> (dev & 63) & 1)) {
     done_mask.fetch_or(1ull << (dev & 63));
     // the narrowest slab has the most positions per tile, i.e. the largest column/value rings
-    CUDA_CHECK(cudaFuncSetAttribute(spmx_dev::spmm_long_row_kernel<C, PIECE>,
+    CUDA_CHECK(cudaFuncSetAttribute(spmx_dev::spmm_long_row_kernel<PIECE>,
                                     cudaFuncAttributeMaxDynamicSharedMemorySize,
                                     (int)spmx_dev::long_row_smem_bytes(1, PIECE)));
   }
-  spmx_dev::spmm_long_row_kernel<C, PIECE>
+  spmx_dev::spmm_long_row_kernel<PIECE>
       <<<p->n_long_rows, spmx_dev::kLongThreads, smem, st>>>(args, p->long_rows);
   post_launch();
 }
@@ -434,11 +434,8 @@ void launch_long_rows(spmx_ctx* ctx, const spmx_plan* p, spmx_dev::SpmmArgs args
   for (int cc = c0; cc < c0 + dw; cc += 128) {  // the ring holds slabs of up to 128 columns
     args.c0 = cc;
     args.dw = std::min(128, c0 + dw - cc);
-    const int cols_per_lane = (args.dw + 31) / 32;
     const bool p4 = piece4 && args.dw % 4 == 0 && cc % 4 == 0;
-    if (cols_per_lane <= 1) p4 ? launch_long_one<1, 4>(p, args, ctx->s_aux) : launch_long_one<1, 1>(p, args, ctx->s_aux);
-    else if (cols_per_lane == 2) p4 ? launch_long_one<2, 4>(p, args, ctx->s_aux) : launch_long_one<2, 1>(p, args, ctx->s_aux);
-    else p4 ? launch_long_one<4, 4>(p, args, ctx->s_aux) : launch_long_one<4, 1>(p, args, ctx->s_aux);
+    p4 ? launch_long_one<4>(p, args, ctx->s_aux) : launch_long_one<1>(p, args, ctx->s_aux);
   }
   CUDA_CHECK(cudaEventRecord(ctx->ev_join, ctx->s_aux));
 }
@@ -611,13 +608,14 @@ spmx_plan* plan_build(spmx_ctx* ctx, const spmx_csr* a, int strategy, unsigned p
     p->dynamic = dynamic != 0;
     p->batch = batch ? batch : 128;
     // Dynamic row dispatch (DispatchCounter, partition.hpp:38-40: workers claim `batch` rows at a
-    // time). Exact-order plans and SPMX_CLAIM_KERNEL run it literally: persistent warps claim
-    // row batches with atomics (spmm_dynamic_kernel), rows are never cut. In the default mode the
-    // same request is served by the row-split work list below: its chunks ARE handed to the SMs
-    // dynamically, by the hardware's CTA scheduler, and long rows can be shared between chunks
-    // (the claim kernel is row-granular: one lane group walks c2's 39 542-nonzero row alone,
-    // 7.4 ms against 0.26 ms).
-    p->claims = p->dynamic && (exact || (flags & SPMX_CLAIM_KERNEL));
+    // time). SPMX_CLAIM_KERNEL runs it literally: persistent warps claim row batches with atomics
+    // (spmm_dynamic_kernel), rows are never cut. Otherwise the same request is served by the
+    // row-split work list below: its chunks ARE handed to the SMs dynamically, by the hardware's
+    // CTA scheduler; in the default mode long rows are shared between chunks, in exact-order
+    // mode they go to spmm_long_row_kernel (the claim kernel is row-granular: one lane group
+    // walks c2's 39 542-nonzero row alone, 7.2 ms against 0.26 / 0.83 ms). The result is the
+    // same either way (bitwise in exact-order mode).
+    p->claims = p->dynamic && (flags & SPMX_CLAIM_KERNEL);
     if (p->claims) {
       p->counter = dev_alloc_async<u64>(ctx, 1);
       CUDA_CHECK(cudaMemsetAsync(p->counter, 0, sizeof(u64), ctx->stream));

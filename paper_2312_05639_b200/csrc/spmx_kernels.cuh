@@ -683,12 +683,12 @@ spmm_dynamic_kernel(const SpmmArgs a) {
 // the gathers are not. One lane group walking a 39 542-nonzero row alone spends ~118 cycles per
 // position (dependent issue latency of a lone warp: column -> address -> gather -> fma), so the
 // plan hands rows of SPMX_LONG_ROW nonzeros or more to this kernel instead: one CTA of 8 warps
-// per row. All 256 threads gather the X rows of the NEXT tile of positions into registers
-// (kLongK loads of PIECE floats per thread in flight: 64 KB per CTA with float4 pieces) while
-// ONE warp consumes the current tile from shared memory in order, lane l owning columns l,
-// l + 32, ...: per position a broadcast LDS for the value, C conflict-free LDS for the X
-// elements and C dependent FFMAs (~8 cycles per position instead of ~118); then the registers
-// are stored to the other buffer. (cp.async would need no registers, but a warp sustains far
+// per row. All 256 threads gather the X rows of the NEXT TWO tiles of positions into registers
+// (2 x kLongK loads of PIECE floats per thread in flight: 64 KB per CTA with float4 pieces) while
+// the consumer warps walk the current tile in shared memory in order, one column per thread:
+// per position a broadcast LDS for the value (amortised over four positions), one conflict-free
+// LDS for the X element and one dependent FFMA (~10-30 cycles per position instead of ~118);
+// then the registers are stored to the other buffer. (cp.async would need no registers, but a warp sustains far
 // fewer LDGSTS than LDG in flight: the same kernel with cp.async ran at ~74 cycles per position.)
 // The result is bitwise the reference's: same operands, same order, one rounding per step.
 struct LongRow {
@@ -703,7 +703,7 @@ __device__ __forceinline__ void lds_v4(unsigned addr, float& a, float& b, float&
   asm volatile("ld.shared.v4.f32 {%0,%1,%2,%3}, [%4];" : "=f"(a), "=f"(b), "=f"(c), "=f"(d) : "r"(addr) : "memory");
 }
 constexpr int kLongThreads = 256;
-constexpr int kLongK = 16;  // loads in flight per thread
+constexpr int kLongK = 8;  // loads per thread and tile; two tiles are in flight (two register sets)
 
 // positions per tile for a slab of dw columns moved in pieces of `piece` floats
 constexpr int kLongMaxTile = 1024;
@@ -711,29 +711,37 @@ __host__ __device__ constexpr int long_row_tile(int dw, int piece) {
   return kLongThreads * kLongK * piece / dw < kLongMaxTile ? kLongThreads * kLongK * piece / dw : kLongMaxTile;
 }
 __host__ __device__ constexpr size_t long_row_smem_bytes(int dw, int piece) {
-  return 2 * (size_t)kLongThreads * kLongK * piece * 4 + 3 * (size_t)((long_row_tile(dw, piece) + 7) & ~3) * 8;
+  return 2 * (size_t)kLongThreads * kLongK * piece * 4 + 4 * (size_t)((long_row_tile(dw, piece) + 7) & ~3) * 8;
 }
 
-// C: columns per consumer lane (slab width <= 32 * C). PIECE: floats per load (4 when X rows are
-// 16-byte aligned and the slab width is a multiple of 4, else 1). The slab width must divide
-// kLongThreads * kLongK * PIECE (the launcher rounds the tile down to whole positions otherwise).
-template <int C, int PIECE>
-__global__ void __launch_bounds__(kLongThreads)
+// PIECE: floats per load (4 when X rows are 16-byte aligned and the slab width is a multiple of
+// 4, else 1). The slab is at most 128 columns wide: warp w (w < ceil(dw / 32)) runs the chains of
+// columns 32 w .. 32 w + 31, one per lane — the columns are independent chains, and a lone warp
+// issues only one dependent instruction every few cycles, so four consumers are four times as
+// fast as one lane holding four columns.
+//
+// Pipeline, iteration t (tile = TP positions): the gathers of tile t + 2 are issued into the
+// register set that tile t's data has just left; tile t is consumed from shared memory by warp 0;
+// tile t + 1 — issued one iteration ago, so it has had a whole iteration to arrive — is stored
+// from the other register set to the other buffer; one barrier. Column indices and values run
+// two tiles further ahead (registers, then a four-slot ring) under the same rule.
+template <int PIECE>
+__global__ void __launch_bounds__(kLongThreads, 2)  // 128 registers: two rows per SM
 spmm_long_row_kernel(const SpmmArgs a, const LongRow* __restrict__ rows) {
   extern __shared__ float4 long_smem4[];
-  const int dw = a.dw, ldx = a.ldx, tid = threadIdx.x, lane = tid & 31;
+  const int dw = a.dw, ldx = a.ldx, tid = threadIdx.x;
+  const int my_col = tid;                       // consumer threads: tid < dw rounded up to a warp
+  const bool consumer = (tid >> 5) < (dw + 31) / 32;
   const int ppr = dw / PIECE;                             // pieces per X row slab
   const int TP = long_row_tile(dw, PIECE);                // whole positions per tile
   const int cvs = (TP + 7) & ~3;                          // stride of the column/value rings (16-byte rows)
   const int tile_floats = kLongThreads * kLongK * PIECE;  // buffer stride (>= TP * dw)
   float* xbuf = reinterpret_cast<float*>(long_smem4);     // [2][tile_floats]
-  u32* cbuf = reinterpret_cast<u32*>(xbuf + 2 * (size_t)tile_floats);  // [3][cvs]
-  float* vbuf = reinterpret_cast<float*>(cbuf + 3 * cvs);                 // [3][cvs]
+  u32* cbuf = reinterpret_cast<u32*>(xbuf + 2 * (size_t)tile_floats);  // [4][cvs]
+  float* vbuf = reinterpret_cast<float*>(cbuf + 4 * cvs);                 // [4][cvs]
   const unsigned xbuf_s = (unsigned)__cvta_generic_to_shared(xbuf);
   const unsigned vbuf_s = (unsigned)__cvta_generic_to_shared(vbuf);
-  unsigned colb[C];  // byte offset of this lane's columns inside an X row slab (clamped)
-#pragma unroll
-  for (int c = 0; c < C; ++c) colb[c] = (unsigned)min(lane + 32 * c, dw - 1) * 4u;
+  const unsigned colb = (unsigned)min(my_col, dw - 1) * 4u;  // byte offset of this thread's column (clamped)
   if (a.abort_flag && *(volatile const int*)a.abort_flag) return;
   const LongRow lr = rows[blockIdx.x];
   const u64 len = lr.j1 - lr.j0;
@@ -752,10 +760,10 @@ spmm_long_row_kernel(const SpmmArgs a, const LongRow* __restrict__ rows) {
     off[k] = (q % ppr) * PIECE;
   }
   typedef VecT<PIECE> Piece;
-  Piece r[kLongK];
+  Piece set0[kLongK], set1[kLongK];
 
   // column indices and values of a tile: loaded into registers (fetch_cv), stored to ring slot
-  // t % 3 later (store_cv), so that nobody waits for them between the two
+  // t % 4 later (store_cv), so that nobody waits for them between the two
   constexpr int kCv = (kLongMaxTile + kLongThreads - 1) / kLongThreads;
   u32 cv_c[kCv];
   float cv_v[kCv];
@@ -774,78 +782,75 @@ spmm_long_row_kernel(const SpmmArgs a, const LongRow* __restrict__ rows) {
     for (int k = 0; k < kCv; ++k) {
       const int i = tid + k * kLongThreads;
       if (i < TP) {
-        cbuf[(t % 3) * cvs + i] = cv_c[k];
-        vbuf[(t % 3) * cvs + i] = cv_v[k];
+        cbuf[(t & 3) * cvs + i] = cv_c[k];
+        vbuf[(t & 3) * cvs + i] = cv_v[k];
       }
     }
   };
-  auto gather = [&](u64 t) {  // X rows of tile t -> registers
-    const u32* cs = cbuf + (t % 3) * cvs;
+  auto gather = [&](u64 t, Piece (&r)[kLongK]) {  // X rows of tile t -> a register set
+    const u32* cs = cbuf + (t & 3) * cvs;
     const u64 left = t < n_tiles ? len - t * TP : 0;
 #pragma unroll
     for (int k = 0; k < kLongK; ++k)
       if (pos[k] < TP && (u64)pos[k] < left)
         r[k] = ld_x<PIECE>(xbase + (size_t)cs[pos[k]] * (size_t)ldx + off[k], 0);
   };
-  auto stash = [&](u64 t) {  // registers -> buffer t & 1
+  auto stash = [&](u64 t, const Piece (&r)[kLongK]) {  // a register set -> buffer t & 1
     float* dst = xbuf + (t & 1) * (size_t)tile_floats;
 #pragma unroll
     for (int k = 0; k < kLongK; ++k)
       if (pos[k] < TP) *reinterpret_cast<Piece*>(dst + (size_t)pos[k] * dw + off[k]) = r[k];
   };
-
-  fetch_cv(0);
-  store_cv(0);
-  fetch_cv(1);
-  store_cv(1);
-  __syncthreads();
-  gather(0);
-  stash(0);
-  __syncthreads();
-
-  float acc[C];
+  float acc = 0.0f;
+  auto consume = [&](u64 t) {
+    // Loads first, then the chain: 8 positions' values and X elements are in registers before
+    // the first of their FFMAs issues. Threads beyond the slab width read the last column again
+    // (no predicates in the loop; their sums are never stored).
+    const unsigned xb = xbuf_s + (unsigned)(t & 1) * (unsigned)tile_floats * 4u + colb;
+    const unsigned vb = vbuf_s + (unsigned)(t & 3) * (unsigned)cvs * 4u;
+    const int npos = (int)min((u64)TP, len - t * TP);
+    const unsigned row_bytes = (unsigned)dw * 4u;
+    int i = 0;
+    for (; i + 8 <= npos; i += 8) {
+      float v[8], xe[8];
+      lds_v4(vb + (unsigned)i * 4u, v[0], v[1], v[2], v[3]);
+      lds_v4(vb + (unsigned)i * 4u + 16u, v[4], v[5], v[6], v[7]);
 #pragma unroll
-  for (int c = 0; c < C; ++c) acc[c] = 0.0f;
-  for (u64 t = 0; t < n_tiles; ++t) {
-    gather(t + 1);    // in flight while tile t is consumed
-    fetch_cv(t + 2);  // likewise
-    if (tid < 32) {
-      // Loads first, then the chain: 8 positions' values and X elements are in registers before
-      // the first of their FFMAs issues. Lanes beyond the slab width read the last column again
-      // (no predicates in the loop; their sums are never stored).
-      const unsigned xb = xbuf_s + (unsigned)(t & 1) * (unsigned)tile_floats * 4u;
-      const unsigned vb = vbuf_s + (unsigned)(t % 3) * (unsigned)cvs * 4u;
-      const int npos = (int)min((u64)TP, len - t * TP);
-      int i = 0;
-      for (; i + 8 <= npos; i += 8) {
-        float v[8], xe[8][C];
-        lds_v4(vb + (unsigned)i * 4u, v[0], v[1], v[2], v[3]);
-        lds_v4(vb + (unsigned)i * 4u + 16u, v[4], v[5], v[6], v[7]);
+      for (int e = 0; e < 8; ++e) xe[e] = lds_f32(xb + (unsigned)(i + e) * row_bytes);
 #pragma unroll
-        for (int e = 0; e < 8; ++e)
-#pragma unroll
-          for (int c = 0; c < C; ++c) xe[e][c] = lds_f32(xb + (unsigned)((i + e) * dw) * 4u + colb[c]);
-#pragma unroll
-        for (int e = 0; e < 8; ++e)
-#pragma unroll
-          for (int c = 0; c < C; ++c) acc[c] = __fmaf_rn(v[e], xe[e][c], acc[c]);
-      }
-      for (; i < npos; ++i) {
-        const float v = lds_f32(vb + (unsigned)i * 4u);
-#pragma unroll
-        for (int c = 0; c < C; ++c) acc[c] = __fmaf_rn(v, lds_f32(xb + (unsigned)(i * dw) * 4u + colb[c]), acc[c]);
-      }
+      for (int e = 0; e < 8; ++e) acc = __fmaf_rn(v[e], xe[e], acc);
     }
-    stash(t + 1);     // buffer (t + 1) & 1: last read as tile t - 1, before the previous barrier
-    store_cv(t + 2);  // slot (t + 2) % 3: last read as tile t - 1
+    for (; i < npos; ++i) acc = __fmaf_rn(lds_f32(vb + (unsigned)i * 4u), lds_f32(xb + (unsigned)i * row_bytes), acc);
+  };
+
+  for (u64 t = 0; t < 3; ++t) { fetch_cv(t); store_cv(t); }
+  __syncthreads();
+  gather(0, set0);
+  stash(0, set0);
+  gather(1, set1);
+  fetch_cv(3);
+  __syncthreads();
+
+  // Every load is issued a whole iteration before its data is stored to shared memory: nobody
+  // waits for memory between two barriers except for what the previous iteration left in flight.
+  for (u64 t = 0; t < n_tiles; t += 2) {
+    // even tile t: its data left set0 (stored before the last barrier); tile t + 1 is in set1
+    store_cv(t + 3);      // fetched during the previous iteration; slot last read as tile t - 1
+    fetch_cv(t + 4);
+    gather(t + 2, set0);
+    if (consumer) consume(t);
+    stash(t + 1, set1);   // buffer (t + 1) & 1: last read as tile t - 1
+    __syncthreads();
+    if (t + 1 >= n_tiles) break;  // CTA-uniform
+    // odd tile t + 1: tile t + 2 is in set0
+    store_cv(t + 4);
+    fetch_cv(t + 5);
+    gather(t + 3, set1);
+    if (consumer) consume(t + 1);
+    stash(t + 2, set0);
     __syncthreads();
   }
-  if (tid < 32) {
-    float* yr = a.y + (size_t)lr.row * (size_t)ldx + a.c0;
-#pragma unroll
-    for (int c = 0; c < C; ++c)
-      if (lane + 32 * c < dw) __stcs(yr + lane + 32 * c, acc[c]);
-  }
+  if (my_col < dw) __stcs(a.y + (size_t)lr.row * (size_t)ldx + a.c0 + my_col, acc);
 }
 
 // Carry fix-up. A row cut by chunk boundaries is summed from the partials of the chunks that

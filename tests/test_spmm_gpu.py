@@ -100,9 +100,10 @@ def test_reference_golden_instances_bitwise(ctx, golden_instances, oracle):
                 y, _ = run(ctx, m, n, g["row_ptr"], g["col"], g["vals"], g["x"], s, t, EXACT)
                 assert np.array_equal(y.view(np.uint32), want.view(np.uint32)), (idx, s, t)
                 assert oracle.checksum(y) == oracle.checksum(want)
-        y, _ = run(ctx, m, n, g["row_ptr"], g["col"], g["vals"], g["x"], "row", 0, EXACT,
-                   dynamic=True, batch=32)
-        assert np.array_equal(y.view(np.uint32), want.view(np.uint32))
+        for fl in (EXACT, EXACT | CLAIM):
+            y, _ = run(ctx, m, n, g["row_ptr"], g["col"], g["vals"], g["x"], "row", 0, fl,
+                       dynamic=True, batch=32)
+            assert np.array_equal(y.view(np.uint32), want.view(np.uint32))
         # acceptance criterion 2: within 1e-5 of spmm_reference (positive data, no cancellation)
         assert oracle.max_relative_error(y, g["y_unfused"]) <= 1e-5
 
@@ -138,9 +139,10 @@ def test_executor_checksum_invariant(ctx, oracle):
             y, _ = run(ctx, 200, 200, z["row_ptr"], z["col"], z["vals"], z["x"], s, t, EXACT)
             assert oracle.checksum(y) == want
     for t in (1, 2, 4, 7):
-        y, _ = run(ctx, 200, 200, z["row_ptr"], z["col"], z["vals"], z["x"], "row", t, EXACT,
-                   dynamic=True, batch=16)
-        assert oracle.checksum(y) == want
+        for fl in (EXACT, EXACT | CLAIM):
+            y, _ = run(ctx, 200, 200, z["row_ptr"], z["col"], z["vals"], z["x"], "row", t, fl,
+                       dynamic=True, batch=16)
+            assert oracle.checksum(y) == want
     # checksum helper of the library agrees with dense.cpp:17-28
     yd = torch.from_numpy(y).cuda()
     assert ctx.checksum(yd) == want
@@ -162,7 +164,7 @@ def test_every_width_against_oracle(ctx, oracle, d):
         assert np.array_equal(y.view(np.uint32), want.view(np.uint32)), (d, s)
         y, p = run(ctx, m, n, rp, col, vals, x, s, 0, 0)
         assert north_star_ok(y, unf, bound), (d, s)
-    y, _ = run(ctx, m, n, rp, col, vals, x, "row", 0, EXACT, dynamic=True, batch=7)
+    y, _ = run(ctx, m, n, rp, col, vals, x, "row", 0, EXACT | CLAIM, dynamic=True, batch=7)
     assert np.array_equal(y.view(np.uint32), want.view(np.uint32))
 
 

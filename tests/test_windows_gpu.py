@@ -73,7 +73,7 @@ def test_window_limits(ctx, oracle, kind, d):
         assert np.array_equal(y.view(np.uint32), fused.view(np.uint32)), (kind, d, strat, parts)
         p.close()
     # dynamic row dispatch (row-granular pieces of 128 rows, several windows for sparse rows)
-    p = ctx.plan(a, "row", 0, dynamic=True, flags=EXACT_ORDER)
+    p = ctx.plan(a, "row", 0, dynamic=True, flags=EXACT_ORDER | 8)  # 8 = SPMX_CLAIM_KERNEL
     yd = torch.full((m, d), float("nan"), device="cuda")
     ctx.spmm(p, a, xd, yd)
     ctx.synchronize()

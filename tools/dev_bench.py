@@ -52,7 +52,9 @@ def main():
         for strat in args.strategies.split(","):
             for mode in args.modes.split(","):
                 flags = {"fast": 0, "exact": EXACT_ORDER, "jit": JIT_WIDTH}[mode]
-                dyn = strat == "row-dyn"
+                dyn = strat in ("row-dyn", "row-claim")  # row-claim: the literal claim kernel
+                if strat == "row-claim":
+                    flags |= 8  # SPMX_CLAIM_KERNEL
                 tp = time.time()
                 p = ctx.plan(da, strat.split("-")[0], args.parts, dynamic=dyn, flags=flags)
                 ctx.synchronize()
