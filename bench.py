@@ -259,10 +259,28 @@ def run_single(args):
     import torch
     from paper_2312_05639_b200.binding import Context, EXACT_ORDER, Lib
 
-    dev = torch.device("cuda", 0)
-    torch.cuda.set_device(0)
     name = args.workload or "c2"
     flags = EXACT_ORDER if args.exact else 0
+    # ---- CPU baseline first: before this process has touched the GPU or pinned any memory ----
+    # It IS the reference arm, run as a child process (python bench.py --impl reference): the same
+    # code, arrays and process conditions as the driver's own reference run. (Measured inside this
+    # process after CUDA start-up and host-buffer pinning, the same run_spmm call took 31-34 ms
+    # instead of 18-23 ms on c2.)
+    cpu = None
+    if not args.no_cpu_baseline:
+        cmd = [sys.executable, os.path.abspath(__file__), "--impl", "reference", "--workload", name,
+               "--strategy", args.strategy, "--steps", "5" if name in ("c1", "c2") else "3", "--warmup", "2"]
+        if args.scale is not None:
+            cmd += ["--scale", str(args.scale)]
+        env = {k: v for k, v in os.environ.items() if k not in ("RANK", "WORLD_SIZE", "LOCAL_RANK")}
+        try:
+            out = subprocess.run(cmd, capture_output=True, text=True, timeout=900, env=env).stdout
+            cpu = json.loads([l for l in out.splitlines() if l.startswith("{")][-1])["cpu_baseline"]
+        except Exception as e:  # the GPU numbers do not depend on it
+            cpu = {"value": None, "unit": UNIT, "error": f"reference arm child failed: {e!r}"}
+
+    dev = torch.device("cuda", 0)
+    torch.cuda.set_device(0)
     lib = Lib.get()
     # everything (generation, kernels, timing events) runs on one explicit torch stream; the
     # legacy default stream has handle 0, which the C ABI reads as "create a private stream"
@@ -280,24 +298,6 @@ def run_single(args):
     y_h = torch.empty(a.m, d, dtype=torch.float32).pin_memory()
     rp_n, col_n = rp_h.numpy().view(np.uint64), col_h.numpy().view(np.uint32)
     vals_n, x_n, y_n = vals_h.numpy(), x_h.numpy(), y_h.numpy()
-
-    # ---- CPU baseline first (nothing of ours is running on the host or the GPU meanwhile) ----
-    # It IS the reference arm, run as a child process (python bench.py --impl reference): the same
-    # code, arrays and process conditions the driver's own reference run has, so the two numbers
-    # agree by construction (measured inside this process, after CUDA start-up and host-buffer
-    # pinning, the same run_spmm call took 31 ms instead of 18 ms on c2).
-    cpu = None
-    if not args.no_cpu_baseline:
-        cmd = [sys.executable, os.path.abspath(__file__), "--impl", "reference", "--workload", name,
-               "--strategy", args.strategy, "--steps", "5" if a.nnz < 80_000_000 else "3", "--warmup", "2"]
-        if args.scale is not None:
-            cmd += ["--scale", str(args.scale)]
-        env = {k: v for k, v in os.environ.items() if k not in ("RANK", "WORLD_SIZE", "LOCAL_RANK")}
-        try:
-            out = subprocess.run(cmd, capture_output=True, text=True, timeout=900, env=env).stdout
-            cpu = json.loads([l for l in out.splitlines() if l.startswith("{")][-1])["cpu_baseline"]
-        except Exception as e:  # the GPU numbers do not depend on it
-            cpu = {"value": None, "unit": UNIT, "error": f"reference arm child failed: {e!r}"}
 
     torch.cuda.empty_cache()  # hand the generator's scratch back: the library allocates with cudaMalloc
     da = ctx.csr_wrap(a)
