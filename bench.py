@@ -565,10 +565,12 @@ def main():
 
     import torch
     assert torch.cuda.is_available(), "bench.py needs a CUDA device: there is no CPU fallback"
-    if world == 1:
+    # SPMX_BENCH_MG=1 (debug): take the multi-GPU driver's path even with one rank, e.g. under
+    # `torchrun --nproc-per-node 1`, to exercise the rendezvous and the rank-mode communicator
+    if world == 1 and os.environ.get("SPMX_BENCH_MG") != "1":
         run_single(args)
     else:
-        run_multi(args, world, rank, local_rank, under_torchrun)
+        run_multi(args, world, rank, local_rank, under_torchrun or "RANK" in os.environ)
 
 
 if __name__ == "__main__":

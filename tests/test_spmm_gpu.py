@@ -401,3 +401,18 @@ def test_row_shards_on_one_device_concatenate_to_the_whole(ctx, oracle):
             else:
                 assert north_star_ok(got, unf, bound), G
     da.close()
+
+
+def test_golden_instances_through_the_long_row_kernel(ctx, golden_instances, monkeypatch):
+    """SPMX_LONG_ROW=8: nearly every row of the reference's acceptance instances is 'long', so the
+    exact-order plans send them through spmm_long_row_kernel (every width of the reference's d
+    pool, scalar and float4 pieces, ragged tiles). Bitwise equal to the reference's run_spmm."""
+    monkeypatch.setenv("SPMX_LONG_ROW", "8")
+    for idx, g in enumerate(golden_instances):
+        m, n, nnz, d = (int(v) for v in g["dims"])
+        for s in STRATS:
+            for t in (0, 3):
+                y, p = run(ctx, m, n, g["row_ptr"], g["col"], g["vals"], g["x"], s, t, EXACT)
+                assert np.array_equal(y.view(np.uint32), g["y_fused"].view(np.uint32)), (idx, s, t, d)
+        y, _ = run(ctx, m, n, g["row_ptr"], g["col"], g["vals"], g["x"], "row", 0, EXACT, dynamic=True)
+        assert np.array_equal(y.view(np.uint32), g["y_fused"].view(np.uint32)), (idx, "dynamic")
