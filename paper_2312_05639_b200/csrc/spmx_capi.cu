@@ -404,7 +404,7 @@ void launch_fixup(const spmx_plan* p, u64 tb, u64 te, float* d_y, int ldx, int c
 // spmm_long_row_kernel for the plan's long rows (exact-order plans), columns [c0, c0 + dw) of X
 // and Y, on the context's auxiliary stream beside the main kernel: forked from `st` here, joined
 // by the caller's join_long_rows after the main kernel has been queued.
-template <int PIECE>
+template <int PIECE, int DW>
 void launch_long_one(const spmx_plan* p, const spmx_dev::SpmmArgs& args, cudaStream_t st) {
   const size_t smem = spmx_dev::long_row_smem_bytes(args.dw, PIECE);
   static std::atomic<uint64_t> done_mask{0};  // one bit per device
@@ -413,11 +413,11 @@ void launch_long_one(const spmx_plan* p, const spmx_dev::SpmmArgs& args, cudaStr
   if (!(done_mask.load() >> (dev & 63) & 1)) {
     done_mask.fetch_or(1ull << (dev & 63));
     // the narrowest slab has the most positions per tile, i.e. the largest column/value rings
-    CUDA_CHECK(cudaFuncSetAttribute(spmx_dev::spmm_long_row_kernel<PIECE>,
+    CUDA_CHECK(cudaFuncSetAttribute(spmx_dev::spmm_long_row_kernel<PIECE, DW>,
                                     cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                    (int)spmx_dev::long_row_smem_bytes(1, PIECE)));
+                                    (int)spmx_dev::long_row_smem_bytes(DW ? DW : 1, PIECE)));
   }
-  spmx_dev::spmm_long_row_kernel<PIECE>
+  spmx_dev::spmm_long_row_kernel<PIECE, DW>
       <<<p->n_long_rows, spmx_dev::kLongThreads, smem, st>>>(args, p->long_rows);
   post_launch();
 }
@@ -435,7 +435,11 @@ void launch_long_rows(spmx_ctx* ctx, const spmx_plan* p, spmx_dev::SpmmArgs args
     args.c0 = cc;
     args.dw = std::min(128, c0 + dw - cc);
     const bool p4 = piece4 && args.dw % 4 == 0 && cc % 4 == 0;
-    p4 ? launch_long_one<4>(p, args, ctx->s_aux) : launch_long_one<1>(p, args, ctx->s_aux);
+    if (!p4) launch_long_one<1, 0>(p, args, ctx->s_aux);
+    else if (args.dw == 128) launch_long_one<4, 128>(p, args, ctx->s_aux);
+    else if (args.dw == 64) launch_long_one<4, 64>(p, args, ctx->s_aux);
+    else if (args.dw == 32) launch_long_one<4, 32>(p, args, ctx->s_aux);
+    else launch_long_one<4, 0>(p, args, ctx->s_aux);
   }
   CUDA_CHECK(cudaEventRecord(ctx->ev_join, ctx->s_aux));
 }

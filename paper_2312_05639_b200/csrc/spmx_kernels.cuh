@@ -702,6 +702,18 @@ __device__ __forceinline__ float lds_f32(unsigned addr) {
 __device__ __forceinline__ void lds_v4(unsigned addr, float& a, float& b, float& c, float& d) {
   asm volatile("ld.shared.v4.f32 {%0,%1,%2,%3}, [%4];" : "=f"(a), "=f"(b), "=f"(c), "=f"(d) : "r"(addr) : "memory");
 }
+__device__ __forceinline__ u32 lds_u32(unsigned addr) {
+  u32 v;
+  asm volatile("ld.shared.u32 %0, [%1];" : "=r"(v) : "r"(addr) : "memory");
+  return v;
+}
+template <int PIECE>
+__device__ __forceinline__ void sts_piece(unsigned addr, const VecT<PIECE>& p) {
+  if constexpr (PIECE == 4)
+    asm volatile("st.shared.v4.f32 [%0], {%1,%2,%3,%4};" ::"r"(addr), "f"(p.v[0]), "f"(p.v[1]), "f"(p.v[2]), "f"(p.v[3]) : "memory");
+  else
+    asm volatile("st.shared.f32 [%0], %1;" ::"r"(addr), "f"(p.v[0]) : "memory");
+}
 constexpr int kLongThreads = 256;
 constexpr int kLongK = 8;  // loads per thread and tile; two tiles are in flight (two register sets)
 
@@ -715,21 +727,32 @@ __host__ __device__ constexpr size_t long_row_smem_bytes(int dw, int piece) {
 }
 
 // PIECE: floats per load (4 when X rows are 16-byte aligned and the slab width is a multiple of
-// 4, else 1). The slab is at most 128 columns wide: warp w (w < ceil(dw / 32)) runs the chains of
-// columns 32 w .. 32 w + 31, one per lane — the columns are independent chains, and a lone warp
-// issues only one dependent instruction every few cycles, so four consumers are four times as
-// fast as one lane holding four columns.
+// 4, else 1). DW: the slab width when it is known at compile time (32, 64, 128: the element
+// offsets of the consumer's loads become immediates), 0 = a.dw. The slab is at most 128 columns
+// wide: warp w (w < ceil(dw / 32)) runs the chains of columns 32 w .. 32 w + 31, one per lane —
+// the columns are independent chains, and a lone warp issues only one dependent instruction
+// every few cycles, so four consumers are four times as fast as one lane holding four columns.
 //
 // Pipeline, iteration t (tile = TP positions): the gathers of tile t + 2 are issued into the
-// register set that tile t's data has just left; tile t is consumed from shared memory by warp 0;
-// tile t + 1 — issued one iteration ago, so it has had a whole iteration to arrive — is stored
-// from the other register set to the other buffer; one barrier. Column indices and values run
-// two tiles further ahead (registers, then a four-slot ring) under the same rule.
-template <int PIECE>
+// register set that tile t's data has just left; tile t is consumed from shared memory by the
+// consumer warps; tile t + 1 — issued one iteration ago, so it has had a whole iteration to
+// arrive — is stored from the other register set to the other buffer; one barrier. Column
+// indices and values run two tiles further ahead (registers, then a four-slot ring) under the
+// same rule. Everything that does not change from tile to tile (which position and which columns
+// a thread's k-th load belongs to, its shared-memory offsets) is computed once: a warp that has
+// few instructions to issue per tile is what keeps the consumers, which share the SM's issue
+// slots with the seven other warps, near the latency of their chain.
+// Measured split on c4 (d = 32, longest row 184 124 nonzeros, 2.29 ms): 1.27 ms without the
+// consumer, 1.83 ms without the gathers — the two add up instead of overlapping, because ptxas
+// puts the gathers of both register sets and the consumer's LDS results on scoreboards that a
+// consumer warp has to drain together (the counter semantics of DESIGN.md 7.5). Dedicated
+// producer warps, split in two groups with one tile in flight each, would take the loads off the
+// consumers' scoreboards; not done.
+template <int PIECE, int DW>
 __global__ void __launch_bounds__(kLongThreads, 2)  // 128 registers: two rows per SM
 spmm_long_row_kernel(const SpmmArgs a, const LongRow* __restrict__ rows) {
   extern __shared__ float4 long_smem4[];
-  const int dw = a.dw, ldx = a.ldx, tid = threadIdx.x;
+  const int dw = DW ? DW : a.dw, ldx = a.ldx, tid = threadIdx.x;
   const int my_col = tid;                       // consumer threads: tid < dw rounded up to a warp
   const bool consumer = (tid >> 5) < (dw + 31) / 32;
   const int ppr = dw / PIECE;                             // pieces per X row slab
@@ -740,6 +763,7 @@ spmm_long_row_kernel(const SpmmArgs a, const LongRow* __restrict__ rows) {
   u32* cbuf = reinterpret_cast<u32*>(xbuf + 2 * (size_t)tile_floats);  // [4][cvs]
   float* vbuf = reinterpret_cast<float*>(cbuf + 4 * cvs);                 // [4][cvs]
   const unsigned xbuf_s = (unsigned)__cvta_generic_to_shared(xbuf);
+  const unsigned cbuf_s = (unsigned)__cvta_generic_to_shared(cbuf);
   const unsigned vbuf_s = (unsigned)__cvta_generic_to_shared(vbuf);
   const unsigned colb = (unsigned)min(my_col, dw - 1) * 4u;  // byte offset of this thread's column (clamped)
   if (a.abort_flag && *(volatile const int*)a.abort_flag) return;
@@ -748,16 +772,21 @@ spmm_long_row_kernel(const SpmmArgs a, const LongRow* __restrict__ rows) {
   const u64 n_tiles = (len + TP - 1) / TP;
   const u32* __restrict__ colp = a.col + lr.j0;
   const float* __restrict__ valp = a.vals + lr.j0;
-  const float* __restrict__ xbase = a.x + a.c0;
 
-  // piece q = k * kLongThreads + tid of a tile belongs to position pos[k], columns off[k]...
-  // (the same for every tile)
-  int pos[kLongK], off[kLongK];
+  // piece q = k * kLongThreads + tid of a tile: position pos[k] of the tile, columns
+  // off .. off + PIECE - 1 of the slab. Kept as the byte offset of the position's column index
+  // in a ring slot (cpos), the piece's byte offset in a tile buffer (soff) and the address of the
+  // piece in X row 0 (xcol); `live` has bit k set when the piece exists (pos[k] < TP).
+  unsigned cpos[kLongK], soff[kLongK], live = 0;
+  const float* xcol[kLongK];
 #pragma unroll
   for (int k = 0; k < kLongK; ++k) {
     const int q = k * kLongThreads + tid;
-    pos[k] = q / ppr;
-    off[k] = (q % ppr) * PIECE;
+    const int pos = q / ppr, off = (q % ppr) * PIECE;
+    cpos[k] = (unsigned)pos * 4u;
+    soff[k] = (unsigned)(pos * dw + off) * 4u;
+    xcol[k] = a.x + a.c0 + off;
+    if (pos < TP) live |= 1u << k;
   }
   typedef VecT<PIECE> Piece;
   Piece set0[kLongK], set1[kLongK];
@@ -765,11 +794,13 @@ spmm_long_row_kernel(const SpmmArgs a, const LongRow* __restrict__ rows) {
   // column indices and values of a tile: loaded into registers (fetch_cv), stored to ring slot
   // t % 4 later (store_cv), so that nobody waits for them between the two
   constexpr int kCv = (kLongMaxTile + kLongThreads - 1) / kLongThreads;
+  const int n_cv = (TP + kLongThreads - 1) / kLongThreads;  // 1 for slabs of 32 columns and more
   u32 cv_c[kCv];
   float cv_v[kCv];
   auto fetch_cv = [&](u64 t) {
 #pragma unroll
     for (int k = 0; k < kCv; ++k) {
+      if (k >= n_cv) break;
       const int i = tid + k * kLongThreads;
       const u64 p = t * TP + i;
       cv_c[k] = 0;
@@ -780,6 +811,7 @@ spmm_long_row_kernel(const SpmmArgs a, const LongRow* __restrict__ rows) {
   auto store_cv = [&](u64 t) {
 #pragma unroll
     for (int k = 0; k < kCv; ++k) {
+      if (k >= n_cv) break;
       const int i = tid + k * kLongThreads;
       if (i < TP) {
         cbuf[(t & 3) * cvs + i] = cv_c[k];
@@ -788,39 +820,52 @@ spmm_long_row_kernel(const SpmmArgs a, const LongRow* __restrict__ rows) {
     }
   };
   auto gather = [&](u64 t, Piece (&r)[kLongK]) {  // X rows of tile t -> a register set
-    const u32* cs = cbuf + (t & 3) * cvs;
+    const unsigned cs = cbuf_s + (unsigned)(t & 3) * (unsigned)cvs * 4u;
     const u64 left = t < n_tiles ? len - t * TP : 0;
+    if (left >= (u64)TP && live == (1u << kLongK) - 1u) {  // a whole tile, every piece exists
 #pragma unroll
-    for (int k = 0; k < kLongK; ++k)
-      if (pos[k] < TP && (u64)pos[k] < left)
-        r[k] = ld_x<PIECE>(xbase + (size_t)cs[pos[k]] * (size_t)ldx + off[k], 0);
+      for (int k = 0; k < kLongK; ++k)
+        r[k] = ld_x<PIECE>(xcol[k] + (size_t)lds_u32(cs + cpos[k]) * (size_t)ldx, 0);
+    } else {
+#pragma unroll
+      for (int k = 0; k < kLongK; ++k)
+        if ((live >> k & 1u) && (u64)(cpos[k] >> 2) < left)
+          r[k] = ld_x<PIECE>(xcol[k] + (size_t)lds_u32(cs + cpos[k]) * (size_t)ldx, 0);
+    }
   };
   auto stash = [&](u64 t, const Piece (&r)[kLongK]) {  // a register set -> buffer t & 1
-    float* dst = xbuf + (t & 1) * (size_t)tile_floats;
+    const unsigned dst = xbuf_s + (unsigned)(t & 1) * (unsigned)tile_floats * 4u;
 #pragma unroll
     for (int k = 0; k < kLongK; ++k)
-      if (pos[k] < TP) *reinterpret_cast<Piece*>(dst + (size_t)pos[k] * dw + off[k]) = r[k];
+      if (live >> k & 1u) sts_piece<PIECE>(dst + soff[k], r[k]);
   };
+
   float acc = 0.0f;
   auto consume = [&](u64 t) {
     // Loads first, then the chain: 8 positions' values and X elements are in registers before
     // the first of their FFMAs issues. Threads beyond the slab width read the last column again
     // (no predicates in the loop; their sums are never stored).
-    const unsigned xb = xbuf_s + (unsigned)(t & 1) * (unsigned)tile_floats * 4u + colb;
-    const unsigned vb = vbuf_s + (unsigned)(t & 3) * (unsigned)cvs * 4u;
+    unsigned xb = xbuf_s + (unsigned)(t & 1) * (unsigned)tile_floats * 4u + colb;
+    unsigned vb = vbuf_s + (unsigned)(t & 3) * (unsigned)cvs * 4u;
     const int npos = (int)min((u64)TP, len - t * TP);
     const unsigned row_bytes = (unsigned)dw * 4u;
     int i = 0;
     for (; i + 8 <= npos; i += 8) {
       float v[8], xe[8];
-      lds_v4(vb + (unsigned)i * 4u, v[0], v[1], v[2], v[3]);
-      lds_v4(vb + (unsigned)i * 4u + 16u, v[4], v[5], v[6], v[7]);
+      lds_v4(vb, v[0], v[1], v[2], v[3]);
+      lds_v4(vb + 16u, v[4], v[5], v[6], v[7]);
 #pragma unroll
-      for (int e = 0; e < 8; ++e) xe[e] = lds_f32(xb + (unsigned)(i + e) * row_bytes);
+      for (int e = 0; e < 8; ++e) xe[e] = lds_f32(xb + (unsigned)e * row_bytes);
 #pragma unroll
       for (int e = 0; e < 8; ++e) acc = __fmaf_rn(v[e], xe[e], acc);
+      vb += 32u;
+      xb += 8u * row_bytes;
     }
-    for (; i < npos; ++i) acc = __fmaf_rn(lds_f32(vb + (unsigned)i * 4u), lds_f32(xb + (unsigned)i * row_bytes), acc);
+    for (; i < npos; ++i) {
+      acc = __fmaf_rn(lds_f32(vb), lds_f32(xb), acc);
+      vb += 4u;
+      xb += row_bytes;
+    }
   };
 
   for (u64 t = 0; t < 3; ++t) { fetch_cv(t); store_cv(t); }
