@@ -7,8 +7,9 @@
 //
 // Mapping: a "group" of G lanes owns one "chunk" of the work list (spmx_plan) — the
 // contiguous piece of the merge path between two (row, nnz) coordinates — and one output
-// row at a time; each lane holds NT x VEC consecutive-column accumulators (d = 32 -> G = 8,
-// NT = 1; d = 64 -> G = 8, NT = 2; d = 128 -> G = 8, NT = 4; VEC = 4: float4 tiles). The
+// row at a time; each lane holds NT x VEC consecutive-column accumulators. G = 8 wherever a row
+// can be spread over eight lanes (d = 8 -> VEC = 1; d = 16 -> VEC = 2; d = 32 -> VEC = 4;
+// d = 64 -> NT = 2 float4 tiles; d = 128 -> NT = 4; see spmx_jit::choose_shape). The
 // 32/G groups of a warp run the same instruction stream on different chunks. Rows that lie
 // wholly inside a chunk are accumulated by a single group in CSR order (bitwise equal to
 // the reference). A row cut by a chunk boundary leaves a partial in carry_out[chunk];
