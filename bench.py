@@ -138,6 +138,19 @@ def describe(name, spec, m, n, nnz, strategy):
             "l2": "inputs exceed L2 (no flush needed)" if name != "c1" else "fits L2"}
 
 
+def host_info():
+    """nproc and the CPU model (BASELINE.md section 4 asks for both with every result)."""
+    model = None
+    try:
+        for line in open("/proc/cpuinfo"):
+            if line.startswith("model name"):
+                model = line.split(":", 1)[1].strip()
+                break
+    except OSError:
+        pass
+    return {"nproc": os.cpu_count(), "cpu": model}
+
+
 def host_threads():
     # all host threads, stated explicitly: torchrun exports OMP_NUM_THREADS=1, which would
     # otherwise make the reference's "threads = 0 -> omp_get_max_threads()" single-threaded
@@ -205,7 +218,7 @@ def run_reference_arm(args, rank, world):
             "config": describe(name, spec, a.m, a.n, a.nnz, strategy),
             "cpu_baseline": cpu,
             "e2e": {"value": cpu["value"], "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
-            "gpu_launches": 0, "host": {"nproc": os.cpu_count()}}
+            "gpu_launches": 0, "host": host_info()}
     print(json.dumps(line), flush=True)
 
 
@@ -228,7 +241,8 @@ def roofline_block(name, args, world, m_total, n_cols, nnz_total, d, ms_step, ga
     except Exception:
         pass
     roofline = {"bound": "hbm", "achieved": achieved, "peak": peak * world, "unit": "GB/s",
-                "frac": achieved / (peak * world), "traffic": traffic, "traffic_source": traffic_src,
+                "frac": achieved / (peak * world), "frac_of_nominal_8tbs": achieved / (8000.0 * world),
+                "traffic": traffic, "traffic_source": traffic_src,
                 "algorithmic_bytes": bytes_alg, "peak_source": peak_src,
                 "kernel": "spmm_chunk_kernel (+ carry_fixup_kernel), one launch pair per step and shard"}
     gather_bytes = 4.0 * nnz_total * d
@@ -365,7 +379,7 @@ def run_single(args):
             "config": describe(name, spec, a.m, a.n, a.nnz, args.strategy),
             "details": {"mode": "exact-order" if args.exact else "default", "build": build_info(lib)},
             "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": launches,
-            "clocks": clocks, "e2e_matches_device_path": same, "host": {"nproc": os.cpu_count()}}
+            "clocks": clocks, "e2e_matches_device_path": same, "host": host_info()}
     print(json.dumps(line), flush=True)
 
 
@@ -529,7 +543,7 @@ def run_multi(args, world, rank, local_rank, under_torchrun):
                 "config": describe(name, spec, m_total, n_cols, nnz_total, args.strategy),
                 "details": dict(details, build=build_info(lib)),
                 "roofline": roofline, "cpu_baseline": None, "e2e": e2e, "gpu_launches": launches,
-                "clocks": clocks, "y_allgather_ms": allgather_ms, "host": {"nproc": os.cpu_count()}}
+                "clocks": clocks, "y_allgather_ms": allgather_ms, "host": host_info()}
         print(json.dumps(line), flush=True)
     mg.close()
     if dist is not None:
