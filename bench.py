@@ -440,6 +440,27 @@ def run_multi(args, world, rank, local_rank, under_torchrun):
     d = spec["d"]
     m_total, n_cols, nnz_total = a.m, a.n, a.nnz
     torch.cuda.synchronize()
+    # The same workload on ONE GPU (rank 0, the unsharded matrix, same strategy and mode), so
+    # that the N-GPU number can be read against its own single-GPU time: the N = 1 bench line is
+    # a different workload (c2, the configuration the metric is quoted on).
+    single = None
+    if rank == 0:
+        from paper_2312_05639_b200.binding import Context
+        sctx = Context.on_torch_stream(local_devs[0]) if not under_torchrun else \
+            Context(local_devs[0], torch.cuda.current_stream().cuda_stream)
+        sda = sctx.csr_wrap(a, validate=False)
+        sy = torch.empty(m_total, d, device=dev0)
+        splan = sctx.plan(sda, args.strategy, 0, flags=flags)
+        for _ in range(2):
+            sctx.spmm(splan, sda, x, sy)
+        ts = [sctx.spmm(splan, sda, x, sy, timed=True) for _ in range(5)]
+        single_ms = float(np.median(ts))
+        single = {"ms_per_step": single_ms, "value": 2.0 * nnz_total * d / (single_ms * 1e-3) / 1e9, "unit": UNIT,
+                  "what": f"{name} unsharded on one GPU (rank 0), median of 5"}
+        splan.close(); sda.close(); sctx.close()
+        del sy
+        torch.cuda.synchronize()
+        torch.cuda.empty_cache()
     ranges = mg.shard_device(a, by=args.shard_by)   # split_nnz(A, G) on the device + placement
     shards = mg.local_shards()
     # X lives on rank 0; every other rank receives it over NVLink in ONE broadcast
@@ -543,7 +564,8 @@ def run_multi(args, world, rank, local_rank, under_torchrun):
                 "config": describe(name, spec, m_total, n_cols, nnz_total, args.strategy),
                 "details": dict(details, build=build_info(lib)),
                 "roofline": roofline, "cpu_baseline": None, "e2e": e2e, "gpu_launches": launches,
-                "clocks": clocks, "y_allgather_ms": allgather_ms, "host": host_info()}
+                "clocks": clocks, "y_allgather_ms": allgather_ms, "single_gpu_same_workload": single,
+                "speedup_vs_single_gpu": (gflops / single["value"]) if single else None, "host": host_info()}
         print(json.dumps(line), flush=True)
     mg.close()
     if dist is not None:
