@@ -463,11 +463,11 @@ def run_multi(args, world, rank, local_rank, under_torchrun):
         torch.cuda.empty_cache()
     ranges = mg.shard_device(a, by=args.shard_by)   # split_nnz(A, G) on the device + placement
     shards = mg.local_shards()
-    # X lives on rank 0; every other rank receives it over NVLink in ONE broadcast
-    xs = [x if (rank == 0 and i == 0) else torch.zeros(n_cols, d, device=torch.device("cuda", dv))
-          for i, dv in enumerate(local_devs)]
+    # X lives on rank 0; every other rank receives it over NVLink in ONE broadcast into replicas
+    # the driver owns (with them it also keeps each rank's hottest X rows compact and L2-resident)
     torch.cuda.synchronize()
-    bcast_ms = reduce([mg.broadcast_x_device(xs, root=0)], "max")[0]
+    copy_ms, bcast_ms = mg.broadcast_x_from_device(x if rank == 0 else None, root=0, shape=(n_cols, d))
+    bcast_ms = reduce([bcast_ms], "max")[0]
     mg.plan(args.strategy, 0, flags=flags)
     details.update({"x_broadcast_ms": bcast_ms,
                     "shard_rows": [[int(b), int(e)] for b, e in ranges],
@@ -526,7 +526,7 @@ def run_multi(args, world, rank, local_rank, under_torchrun):
         mg.download_y_shards(y_dev)  # the device-resident result, for the same-bits check below
         rp_n, col_n, vals_n = rp_h.numpy().view(np.uint64), col_h.numpy().view(np.uint32), vals_h.numpy()
         x_n = x_h.numpy() if x_h is not None else None
-        del a, x, xs
+        del a, x
         torch.cuda.empty_cache()
         mg.set_x_shape(n_cols, d)
 

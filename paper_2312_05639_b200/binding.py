@@ -165,6 +165,7 @@ class Lib:
         L.spmx_mg_plan.argtypes = [vp, C.c_int, C.c_uint, C.c_int, u64, C.c_uint]
         L.spmx_mg_broadcast_x_host.argtypes = [vp, vp, C.c_int, i64, i64, fp, fp]
         L.spmx_mg_broadcast_x_device.argtypes = [vp, P(vp), C.c_int, i64, i64, fp]
+        L.spmx_mg_broadcast_x_from_device.argtypes = [vp, vp, C.c_int, i64, i64, fp, fp]
         L.spmx_mg_spmm.argtypes = [vp, C.c_int, fp, fp]
         L.spmx_mg_y_shard.argtypes = [vp, C.c_int, P(vp)]
         L.spmx_mg_download_y.argtypes = [vp, vp]
@@ -555,6 +556,20 @@ class MultiGpu:
         self._keep = list(xs)
         self._shape = (rows, d)
         return bc.value
+
+    def broadcast_x_from_device(self, x, root=0, shape=None):
+        """x: the root's N x d tensor on the root's GPU (None on processes that do not drive the
+        root; pass shape=(N, d) there). The driver owns the replicas. Returns (copy_ms, bcast_ms)."""
+        cp, bc = C.c_float(), C.c_float()
+        if x is not None:
+            self._shape = tuple(x.shape)
+            self._keep = [x]
+        elif shape is not None:
+            self._shape = tuple(shape)
+        rows, d = self._shape
+        self.L.check(self.L.lib.spmx_mg_broadcast_x_from_device(self.h, _ptr(x) if x is not None else 0, root,
+                                                                rows, d, C.byref(cp), C.byref(bc)))
+        return cp.value, bc.value
 
     def spmm(self, steps=1, per_shard=False):
         ms = C.c_float()

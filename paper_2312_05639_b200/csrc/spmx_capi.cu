@@ -108,6 +108,7 @@ struct spmx_ctx {
   cudaEvent_t ev0 = nullptr, ev1 = nullptr;
   int* d_err = nullptr;  // device-side error flag for validation
   cudaStream_t s_compute = nullptr, s_d2h = nullptr, s_x = nullptr;  // spmx_spmm_host pipeline (lazy)
+  size_t l2_persist = 0;         // persisting-L2 set-aside this context last asked for (spmx_ctx_l2_window)
   cudaStream_t s_aux = nullptr;  // long rows of exact-order plans run beside the main kernel (lazy)
   cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
   std::vector<cudaEvent_t> pipe_events;                // created once, reused by every call
@@ -1441,7 +1442,11 @@ int spmx_ctx_l2_window(spmx_ctx* ctx, const void* base, size_t bytes, float hit_
     cudaStreamAttrValue v{};
     if (base && bytes) {
       const size_t win = std::min<size_t>(bytes, (size_t)max_window);
-      CUDA_CHECK(cudaDeviceSetLimit(cudaLimitPersistingL2CacheSize, std::min<size_t>(win, (size_t)max_persist)));
+      const size_t want = std::min<size_t>(win, (size_t)max_persist);
+      if (want != ctx->l2_persist) {  // (changing the set-aside reconfigures the L2: tens of milliseconds)
+        CUDA_CHECK(cudaDeviceSetLimit(cudaLimitPersistingL2CacheSize, want));
+        ctx->l2_persist = want;
+      }
       v.accessPolicyWindow.base_ptr = const_cast<void*>(base);
       v.accessPolicyWindow.num_bytes = win;
       v.accessPolicyWindow.hitRatio = hit_ratio;
@@ -1453,9 +1458,10 @@ int spmx_ctx_l2_window(spmx_ctx* ctx, const void* base, size_t bytes, float hit_
       if (out_window_bytes) *out_window_bytes = 0;
     }
     CUDA_CHECK(cudaStreamSetAttribute(ctx->stream, cudaStreamAttributeAccessPolicyWindow, &v));
-    if (!(base && bytes)) {
+    if (!(base && bytes) && ctx->l2_persist != 0) {
       CUDA_CHECK(cudaCtxResetPersistingL2Cache());
       CUDA_CHECK(cudaDeviceSetLimit(cudaLimitPersistingL2CacheSize, 0));
+      ctx->l2_persist = 0;
     }
   });
 }

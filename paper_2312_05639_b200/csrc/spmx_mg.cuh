@@ -91,6 +91,64 @@ __global__ void rebase_row_ptr_kernel(u64* __restrict__ rp, u64 count, u64 base)
   for (u64 i = (u64)blockIdx.x * blockDim.x + threadIdx.x; i < count; i += stride) rp[i] -= base;
 }
 
+// ---- hot X rows (L2 residency for matrices whose X is far larger than the L2) ---------------
+// On a power-law matrix a few columns carry a large share of the nonzeros (c5: the 50 000
+// hottest of 16.8 M columns 43.5 %), yet their X rows are scattered and get evicted by the
+// stream of cold rows (L2 hit 28 %, DRAM traffic 4.9 x the algorithmic bytes). When the driver
+// owns the X replicas it keeps a COMPACT COPY of each rank's hottest rows behind X (rows
+// N .. N + H of the same buffer), points the shards' column indices of those columns at the
+// copy (col' = N + slot: the kernels are unchanged, values and order too) and puts a persisting
+// L2 access-policy window over it. Measured upper bound (tools/exp_hot_window.py, c5): DRAM reads
+// 85.7 -> 75.2 GB, 14.0 -> 12.5 ms.
+__global__ void col_degree_kernel(const uint32_t* __restrict__ col, u64 nnz, uint32_t* __restrict__ deg) {
+  const u64 stride = (u64)gridDim.x * blockDim.x;
+  for (u64 k = (u64)blockIdx.x * blockDim.x + threadIdx.x; k < nnz; k += stride) atomicAdd(deg + col[k], 1u);
+}
+__global__ void count_ge_kernel(const uint32_t* __restrict__ deg, u64 n, uint32_t thr, unsigned long long* out) {
+  const u64 stride = (u64)gridDim.x * blockDim.x;
+  unsigned long long c = 0;
+  for (u64 i = (u64)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += stride) c += deg[i] >= thr;
+  c = __reduce_add_sync(0xffffffffu, (unsigned)c);
+  if ((threadIdx.x & 31) == 0 && c) atomicAdd(out, c);
+}
+// deg[c] becomes the slot of column c (kNotHot when it is not hot); hot_cols[slot] = c
+constexpr uint32_t kNotHot = 0xffffffffu;
+__global__ void assign_slots_kernel(uint32_t* __restrict__ deg, u64 n, uint32_t thr, uint32_t cap,
+                                    uint32_t* __restrict__ hot_cols, uint32_t* __restrict__ counter) {
+  const u64 stride = (u64)gridDim.x * blockDim.x;
+  for (u64 i = (u64)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += stride) {
+    uint32_t slot = kNotHot;
+    if (deg[i] >= thr) {
+      slot = atomicAdd(counter, 1u);
+      if (slot < cap) hot_cols[slot] = (uint32_t)i; else slot = kNotHot;
+    }
+    deg[i] = slot;
+  }
+}
+__global__ void remap_cols_kernel(uint32_t* __restrict__ col, u64 nnz, const uint32_t* __restrict__ slot_of,
+                                  uint32_t n) {
+  const u64 stride = (u64)gridDim.x * blockDim.x;
+  for (u64 k = (u64)blockIdx.x * blockDim.x + threadIdx.x; k < nnz; k += stride) {
+    const uint32_t s = slot_of[col[k]];
+    if (s != kNotHot) col[k] = n + s;
+  }
+}
+__global__ void unmap_cols_kernel(uint32_t* __restrict__ col, u64 nnz, const uint32_t* __restrict__ hot_cols,
+                                  uint32_t n) {
+  const u64 stride = (u64)gridDim.x * blockDim.x;
+  for (u64 k = (u64)blockIdx.x * blockDim.x + threadIdx.x; k < nnz; k += stride)
+    if (col[k] >= n) col[k] = hot_cols[col[k] - n];
+}
+// xext[n + s] = x[hot_cols[s]] for every slot s: d floats per row, one thread per element
+__global__ void compact_rows_kernel(float* __restrict__ x, const uint32_t* __restrict__ hot_cols, u64 n_hot,
+                                    u64 n, int d) {
+  const u64 idx = (u64)blockIdx.x * blockDim.x + threadIdx.x;
+  if (idx >= n_hot * (u64)d) return;
+  const u64 s = idx / (u64)d;
+  const int j = (int)(idx % (u64)d);
+  x[(n + s) * (u64)d + j] = x[(u64)hot_cols[s] * (u64)d + j];
+}
+
 struct MgRank {  // one GPU driven by this process
   int rank = 0;  // global rank
   int device = 0;
@@ -102,6 +160,11 @@ struct MgRank {  // one GPU driven by this process
   float* y_full = nullptr;  // all-gather target (M x d)
   size_t y_full_floats = 0;
   double* red = nullptr;  // scratch of the statistics all-reduce
+  uint32_t* hot_cols = nullptr;  // original column of every hot slot
+  uint32_t* slot_of = nullptr;   // slot of every column (kNotHot), kept while the shards can be remapped
+  uint32_t n_hot = 0;
+  bool remapped = false;         // the rank's shards point their hot columns at rows N .. N + n_hot of X
+  bool window = false;
   cudaEvent_t ev0 = nullptr, ev1 = nullptr;
   float ms = 0.f;
 };
@@ -187,6 +250,15 @@ void mg_free_shards(spmx_mg* g) {
   }
   g->shards.clear();
   g->ranges.clear();
+  for (MgRank& r : g->ranks) {  // the hot-row tables describe the shards that just went away
+    if (!r.ctx) continue;
+    cudaSetDevice(r.device);
+    if (r.hot_cols) cudaFree(r.hot_cols);
+    if (r.slot_of) cudaFree(r.slot_of);
+    r.hot_cols = r.slot_of = nullptr;
+    r.n_hot = 0;
+    r.remapped = false;
+  }
 }
 
 void mg_free(spmx_mg* g) {
@@ -201,6 +273,8 @@ void mg_free(spmx_mg* g) {
     if (r.x && r.x_owned) cudaFree(r.x);
     if (r.y_full) cudaFree(r.y_full);
     if (r.red) cudaFree(r.red);
+    if (r.hot_cols) cudaFree(r.hot_cols);
+    if (r.slot_of) cudaFree(r.slot_of);
     if (r.ev0) cudaEventDestroy(r.ev0);
     if (r.ev1) cudaEventDestroy(r.ev1);
     if (r.ctx) spmx_ctx_destroy(r.ctx);
@@ -313,8 +387,14 @@ void mg_check_shape(int64_t m, int64_t n, int64_t nnz, int shard_by) {
     throw InvalidArg("spmx_mg_shard: shard_by must be SPMX_SHARD_BY_NNZ or SPMX_SHARD_BY_MERGE");
 }
 
+// knobs of the hot-row copy: rows kept per rank (0 disables), and how large X has to be before
+// the persisting L2 window is worth its set-aside (it costs the rest of the L2 what it gives)
+inline u64 mg_hot_rows() { return env_u64("SPMX_MG_HOT_ROWS", 50000); }
+inline u64 mg_hot_min_x_mb() { return env_u64("SPMX_MG_HOT_MIN_MB", 1024); }
+
 void mg_ensure_x(spmx_mg* g, int64_t x_rows, int64_t d) {
-  const size_t need = (size_t)x_rows * (size_t)d;
+  // (room for the compact copy of the hot rows behind X, whatever the current shards need)
+  const size_t need = ((size_t)x_rows + (size_t)mg_hot_rows()) * (size_t)d;
   for (MgRank& r : g->ranks) {
     CUDA_CHECK(cudaSetDevice(r.device));
     if (!r.x_owned) { r.x = nullptr; r.x_floats = 0; }
@@ -325,6 +405,110 @@ void mg_ensure_x(spmx_mg* g, int64_t x_rows, int64_t d) {
       r.x_floats = need;
     }
     r.x_owned = true;
+  }
+}
+
+// Per rank: the H columns with the most nonzeros in the rank's shards (degree histogram, then
+// the smallest threshold that admits at most H columns), their slots, and the list of hot columns.
+void mg_build_hot(spmx_mg* g) {
+  const u64 cap = mg_hot_rows();
+  if (cap == 0 || (u64)g->n < 8 * cap || g->n >= (int64_t)0x7fffffff - (int64_t)cap) return;
+  for (size_t lr = 0; lr < g->ranks.size(); ++lr) {
+    MgRank& r = g->ranks[lr];
+    u64 nnz = 0;
+    for (const MgShard& s : g->shards)
+      if (s.local_rank == (int)lr) nnz += s.nnz;
+    if (nnz == 0) continue;
+    CUDA_CHECK(cudaSetDevice(r.device));
+    cudaStream_t st = r.ctx->stream;
+    const u64 n = (u64)g->n;
+    r.slot_of = dev_alloc<uint32_t>((size_t)n);
+    r.hot_cols = dev_alloc<uint32_t>((size_t)cap);
+    CUDA_CHECK(cudaMemsetAsync(r.slot_of, 0, (size_t)n * 4, st));
+    for (const MgShard& s : g->shards)
+      if (s.local_rank == (int)lr && s.nnz) {
+        col_degree_kernel<<<validate_grid(r.ctx, s.nnz), 256, 0, st>>>(s.csr->col, s.nnz, r.slot_of);
+        post_launch();
+      }
+    unsigned long long* d_cnt = dev_alloc<unsigned long long>(1);
+    uint32_t* d_n = dev_alloc<uint32_t>(1);
+    try {
+      auto count_ge = [&](uint32_t thr) {
+        unsigned long long c = 0;
+        CUDA_CHECK(cudaMemsetAsync(d_cnt, 0, 8, st));
+        count_ge_kernel<<<validate_grid(r.ctx, n), 256, 0, st>>>(r.slot_of, n, thr, d_cnt);
+        post_launch();
+        CUDA_CHECK(cudaMemcpyAsync(&c, d_cnt, 8, cudaMemcpyDeviceToHost, st));
+        CUDA_CHECK(cudaStreamSynchronize(st));
+        return (u64)c;
+      };
+      uint32_t lo = 1, hi = 0x80000000u;  // smallest thr in [lo, hi] with count(deg >= thr) <= cap
+      while (lo < hi) {
+        const uint32_t mid = lo + (hi - lo) / 2;
+        if (count_ge(mid) <= cap) hi = mid; else lo = mid + 1;
+      }
+      CUDA_CHECK(cudaMemsetAsync(d_n, 0, 4, st));
+      assign_slots_kernel<<<validate_grid(r.ctx, n), 256, 0, st>>>(r.slot_of, n, lo, (uint32_t)cap, r.hot_cols, d_n);
+      post_launch();
+      CUDA_CHECK(cudaMemcpyAsync(&r.n_hot, d_n, 4, cudaMemcpyDeviceToHost, st));
+      CUDA_CHECK(cudaStreamSynchronize(st));
+      r.n_hot = std::min<uint32_t>(r.n_hot, (uint32_t)cap);
+    } catch (...) {
+      cudaFree(d_cnt);
+      cudaFree(d_n);
+      throw;
+    }
+    CUDA_CHECK(cudaFree(d_cnt));
+    CUDA_CHECK(cudaFree(d_n));
+  }
+}
+
+// Points the hot columns of every local shard at the compact copy (on) or back at X (off).
+void mg_set_remap(spmx_mg* g, bool on) {
+  for (size_t lr = 0; lr < g->ranks.size(); ++lr) {
+    MgRank& r = g->ranks[lr];
+    if (r.n_hot == 0 || r.remapped == on) continue;
+    CUDA_CHECK(cudaSetDevice(r.device));
+    for (MgShard& s : g->shards) {
+      if (s.local_rank != (int)lr || s.nnz == 0) continue;
+      if (on)
+        remap_cols_kernel<<<validate_grid(r.ctx, s.nnz), 256, 0, r.ctx->stream>>>(s.csr->col, s.nnz, r.slot_of,
+                                                                                  (uint32_t)g->n);
+      else
+        unmap_cols_kernel<<<validate_grid(r.ctx, s.nnz), 256, 0, r.ctx->stream>>>(s.csr->col, s.nnz, r.hot_cols,
+                                                                                  (uint32_t)g->n);
+      post_launch();
+    }
+    r.remapped = on;
+  }
+}
+
+void mg_clear_window(MgRank& r) {
+  if (!r.window) return;
+  CUDA_CHECK(cudaSetDevice(r.device));
+  if (spmx_ctx_l2_window(r.ctx, nullptr, 0, 0.f, nullptr) != SPMX_OK) throw std::runtime_error(g_last_error);
+  r.window = false;
+}
+
+// The driver owns X (x_rows x d at the front of every rank's buffer, just broadcast): refresh the
+// compact copy of the hot rows behind it, point the shards at it, and protect it in L2 when X is
+// large enough for that to pay.
+void mg_refresh_hot(spmx_mg* g, int64_t x_rows, int64_t d) {
+  mg_set_remap(g, true);
+  const bool big = (u64)x_rows * (u64)d * 4 >= (mg_hot_min_x_mb() << 20);
+  for (MgRank& r : g->ranks) {
+    if (r.n_hot == 0) { mg_clear_window(r); continue; }
+    CUDA_CHECK(cudaSetDevice(r.device));
+    const u64 elems = (u64)r.n_hot * (u64)d;
+    compact_rows_kernel<<<blocks_for(elems), 256, 0, r.ctx->stream>>>(r.x, r.hot_cols, r.n_hot, (u64)x_rows, (int)d);
+    post_launch();
+    if (big) {
+      if (spmx_ctx_l2_window(r.ctx, r.x + (size_t)x_rows * (size_t)d, (size_t)elems * 4, 1.0f, nullptr) != SPMX_OK)
+        throw std::runtime_error(g_last_error);
+      r.window = true;
+    } else {
+      mg_clear_window(r);
+    }
   }
 }
 
@@ -499,6 +683,8 @@ int spmx_mg_shard_host(spmx_mg* mg, int64_t m, int64_t n, int64_t nnz, const uin
       };
       // the split has validated row_ptr, so these reads stay inside [0, nnz]
       mg_place(mg, fetch, [&](u64 r) { return (u64)row_ptr[r]; });
+      mg_build_hot(mg);
+      if (mg->d > 0 && mg->ranks[0].x_owned) mg_refresh_hot(mg, n, mg->d);  // X stays across a re-shard
     } catch (...) {
       mg_free_shards(mg);
       throw;
@@ -546,6 +732,8 @@ int spmx_mg_shard_device(spmx_mg* mg, int src_local_rank, int64_t m, int64_t n, 
           CUDA_CHECK(cudaMemcpyPeerAsync(dst, r.device, from, src.device, bytes, r.ctx->stream));
       };
       mg_place(mg, fetch, nnz_at);
+      mg_build_hot(mg);
+      if (mg->d > 0 && mg->ranks[0].x_owned) mg_refresh_hot(mg, n, mg->d);  // X stays across a re-shard
     } catch (...) {
       mg_free_shards(mg);
       throw;
@@ -605,6 +793,31 @@ int spmx_mg_broadcast_x_host(spmx_mg* mg, const float* x_host, int root_rank, in
     }
     mg_broadcast(mg, root_rank, (size_t)x_rows * (size_t)d, bcast_ms);
     mg->d = d;
+    mg_refresh_hot(mg, x_rows, d);
+  });
+}
+
+int spmx_mg_broadcast_x_from_device(spmx_mg* mg, const float* d_x_root, int root_rank, int64_t x_rows,
+                                    int64_t d, float* copy_ms, float* bcast_ms) {
+  return guarded([&] {
+    check(mg);
+    mg_require_x_shape(mg, root_rank, x_rows, d);
+    mg_ensure_x(mg, x_rows, d);
+    if (copy_ms) *copy_ms = 0.f;
+    for (MgRank& r : mg->ranks) {
+      if (r.rank != root_rank) continue;
+      if (!d_x_root && x_rows > 0) throw InvalidArg("run_spmm: null X on the root rank");
+      CUDA_CHECK(cudaSetDevice(r.device));
+      CUDA_CHECK(cudaEventRecord(r.ev0, r.ctx->stream));
+      CUDA_CHECK(cudaMemcpyAsync(r.x, d_x_root, (size_t)x_rows * (size_t)d * 4, cudaMemcpyDeviceToDevice,
+                                 r.ctx->stream));
+      CUDA_CHECK(cudaEventRecord(r.ev1, r.ctx->stream));
+      CUDA_CHECK(cudaEventSynchronize(r.ev1));
+      if (copy_ms) CUDA_CHECK(cudaEventElapsedTime(copy_ms, r.ev0, r.ev1));
+    }
+    mg_broadcast(mg, root_rank, (size_t)x_rows * (size_t)d, bcast_ms);
+    mg->d = d;
+    mg_refresh_hot(mg, x_rows, d);
   });
 }
 
@@ -614,6 +827,8 @@ int spmx_mg_broadcast_x_device(spmx_mg* mg, float* const* d_x_local, int root_ra
     check(mg);
     mg_require_x_shape(mg, root_rank, x_rows, d);
     if (!d_x_local) throw InvalidArg("spmx_mg_broadcast_x_device: null buffer list");
+    mg_set_remap(mg, false);  // borrowed buffers have no room for the compact copy of the hot rows
+    for (MgRank& r : mg->ranks) mg_clear_window(r);
     for (size_t i = 0; i < mg->ranks.size(); ++i) {
       MgRank& r = mg->ranks[i];
       if (!d_x_local[i] && x_rows > 0) throw InvalidArg("run_spmm: null X");

@@ -181,3 +181,41 @@ def test_errors(small_c5):
     with pytest.raises(SpmxInvalidArgument, match="column index out of range"):
         mg.shard_device(a_bad)
     mg.close()
+
+
+@pytest.mark.parametrize("G", [1, 3])
+def test_hot_row_copy_keeps_results_bitwise(small_c5, truth, oracle, monkeypatch, G):
+    """With driver-owned X replicas every rank keeps a compact copy of its hottest X rows behind
+    X, remaps those columns of its shards to the copy and puts an L2 window over it
+    (SPMX_MG_HOT_ROWS; forced on here for a small matrix). Values and order are untouched, so
+    exact-order results stay bitwise equal to the oracle — through the host and the device
+    entry, after switching to borrowed X buffers (remap undone) and back, and across a re-shard."""
+    from paper_2312_05639_b200.binding import MultiGpu
+    monkeypatch.setenv("SPMX_MG_HOT_ROWS", "300")
+    monkeypatch.setenv("SPMX_MG_HOT_MIN_MB", "0")
+    a, x, spec = small_c5
+    want = truth["fused"].view(np.uint32)
+    mg = MultiGpu([0], n_shards=G)
+    mg.shard_device(a, by="nnz")
+
+    def check(tag):
+        for strat, flags in (("merge", EXACT), ("row", EXACT), ("nnz", 0)):
+            mg.plan(strat, 0, flags=flags)
+            mg.spmm(steps=2)
+            got = mg.download_y(m=a.m)
+            if flags:
+                assert np.array_equal(got.view(np.uint32), want), (tag, strat)
+            else:
+                assert north_star_ok(got, truth["unf"], truth["bound"]), (tag, strat)
+
+    mg.broadcast_x_host(truth["xn"], root=0)          # owned: hot copy + remap + window
+    check("host")
+    mg.broadcast_x_device([x], root=0)                # borrowed: remap undone
+    check("borrowed")
+    cp, bc = mg.broadcast_x_from_device(x, root=0)    # owned again, X from the device
+    assert cp > 0
+    check("from_device")
+    mg.shard_host(a.m, a.n, truth["rp"], truth["col"], truth["vals"], by="merge")  # re-shard, X stays
+    check("reshard")
+    mg.allgather_y()
+    mg.close()
