@@ -60,6 +60,30 @@ def generate_kernel_source_include() -> None:
             f.write(text)
 
 
+# nvcc releases whose SASS the post-link scheduling edit has been validated on (encoding of the
+# control words, the walk loop's shape; tests/test_sass_ab_gpu.py is the bitwise A/B check)
+VALIDATED_NVCC = ("12.9",)
+
+
+def _nvcc_validated(verbose: bool) -> bool:
+    """The edit rewrites undocumented scheduling fields: it is applied only under a compiler
+    release it was validated with (SPMX_SASS_SCHED_ANY_NVCC=1 overrides; the preconditions and the
+    A/B test still guard it). Under any other release the kernels ship as compiled."""
+    if os.environ.get("SPMX_SASS_SCHED_ANY_NVCC"):
+        return True
+    try:
+        out = subprocess.run(["nvcc", "--version"], capture_output=True, text=True, check=True).stdout
+    except Exception:
+        return False
+    import re
+    m = re.search(r"release (\d+\.\d+)", out)
+    ok = bool(m) and m.group(1) in VALIDATED_NVCC
+    if not ok and verbose:
+        print(f"sass_sched: nvcc release {m.group(1) if m else '?'} is not in {VALIDATED_NVCC}: kernels are "
+              "shipped as compiled (SPMX_SASS_SCHED_ANY_NVCC=1 to apply the edit anyway)", file=sys.stderr)
+    return ok
+
+
 def build_library(force: bool = False, verbose: bool = False) -> str:
     """Compile csrc/*.cu into libspmx_b200.so for sm_100a (nvcc cross-compiles without a GPU)."""
     srcs = [os.path.join(CSRC, f) for f in sorted(os.listdir(CSRC)) if f.endswith(".cu")]
@@ -77,7 +101,7 @@ def build_library(force: bool = False, verbose: bool = False) -> str:
     shutil.copyfile(LIB_PATH, ASBUILT_PATH)
     # second scoreboard for half of the walk loop's gathers (sass_sched.py):
     # applied only when its preconditions hold, SPMX_NO_SASS_SCHED=1 leaves the kernels as compiled
-    if not os.environ.get("SPMX_NO_SASS_SCHED"):
+    if not os.environ.get("SPMX_NO_SASS_SCHED") and _nvcc_validated(verbose):
         from . import sass_sched
         say = (lambda m: print("sass_sched:", m, file=sys.stderr)) if verbose else (lambda m: None)
         # strict: a precompiled width whose preconditions fail stops the build (a silent
