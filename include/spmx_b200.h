@@ -192,6 +192,11 @@ int spmx_jit_available(void);
 int spmx_ctx_l2_window(spmx_ctx* ctx, const void* base, size_t bytes, float hit_ratio,
                        size_t* out_window_bytes);
 
+/* Self-check builds only (-DSPMX_DEBUG_BOUNDS=1, tools/bounds_check.py): per-site counts of
+ * out-of-bounds accesses the SpMM kernels would have made (all zero = clean). A regular build
+ * answers SPMX_ELOGIC. compute-sanitizer is not available on the GPU pool this was developed on. */
+int spmx_debug_bounds(uint64_t* out16);
+
 /* Measurement aid (bench.py roofline.gather): the L2 -> SM ceiling of this GPU at its current
  * clocks — random 256-byte rows of an L2-resident 64 MB buffer read by 8-lane groups with
  * LDG.128 (the SpMM's own access shape at d = 64), at 24, 32, 40 and 48 warps per SM; the best of

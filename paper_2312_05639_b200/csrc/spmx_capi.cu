@@ -153,6 +153,7 @@ struct spmx_plan {
   spmx_dev::LongRow* long_rows = nullptr;  // exact-order plans: rows run by spmm_long_row_kernel
   uint32_t n_long_rows = 0;
   u64* counter = nullptr;    // dynamic dispatch
+  u64 x_extra_rows = 0;  // rows behind X the columns may point at (the multi-GPU driver's hot-row copy)
   bool may_carry = false;
   mutable float* carry = nullptr;  // n_chunks x ld floats, grown on demand
   mutable size_t carry_floats = 0;
@@ -482,6 +483,8 @@ void run_kernels(spmx_ctx* ctx, const spmx_plan* p, const spmx_csr* a, const flo
   args.chunk_end = ce;
   args.abort_flag = abort_flag;
   args.m = (u64)a->m;
+  args.n_x = (u64)a->n + p->x_extra_rows;
+  args.nnz = (u64)a->nnz;
   args.ldx = (int)d;
   args.counter = p->counter;
   args.batch = p->batch;
@@ -1463,6 +1466,20 @@ int spmx_ctx_l2_window(spmx_ctx* ctx, const void* base, size_t bytes, float hit_
       CUDA_CHECK(cudaDeviceSetLimit(cudaLimitPersistingL2CacheSize, 0));
       ctx->l2_persist = 0;
     }
+  });
+}
+
+int spmx_debug_bounds(uint64_t* out16) {
+  return guarded([&] {
+#if SPMX_DEBUG_BOUNDS
+    unsigned long long h[16];
+    CUDA_CHECK(cudaDeviceSynchronize());
+    CUDA_CHECK(cudaMemcpyFromSymbol(h, spmx_dev::g_bounds_violations, sizeof h));
+    for (int i = 0; i < 16; ++i) out16[i] = h[i];
+#else
+    (void)out16;
+    throw LogicErr("spmx_debug_bounds: this library was not built with -DSPMX_DEBUG_BOUNDS=1");
+#endif
   });
 }
 

@@ -30,6 +30,20 @@ typedef unsigned long long u64;
 typedef unsigned int u32;
 
 constexpr unsigned kFullMask = 0xffffffffu;
+
+// Bounds self-check build (-DSPMX_DEBUG_BOUNDS=1, tools/bounds_check.py): compute-sanitizer is not
+// available on the GPU pool, so every global and shared access of the SpMM kernels is checked
+// against the extents passed in SpmmArgs and violations are counted per site. Off by default:
+// the checks cost instructions in the hot loop.
+#ifndef SPMX_DEBUG_BOUNDS
+#define SPMX_DEBUG_BOUNDS 0
+#endif
+#if SPMX_DEBUG_BOUNDS
+__device__ unsigned long long g_bounds_violations[16];
+#define SPMX_CHECK(cond, site) do { if (!(cond)) atomicAdd(&g_bounds_violations[site], 1ull); } while (0)
+#else
+#define SPMX_CHECK(cond, site) do { } while (0)
+#endif
 #ifndef SPMX_WARPS_PER_CTA
 #define SPMX_WARPS_PER_CTA 2  // small CTAs: a finished warp frees its slot at once (measured best)
 #endif
@@ -185,6 +199,7 @@ struct SpmmArgs {
   u64 chunk_end;
   const int* abort_flag;  // when non-null and set (invalid input found on the device): do nothing
   u64 m;
+  u64 n_x, nnz;  // rows of X and nonzeros of A (read by the bounds self-check build only)
   int ldx;     // row stride of X, Y and carry_out in floats (= d)
   int c0;      // first column of the slab this launch computes
   int dw;      // slab width in columns (<= G*VEC*NT)
@@ -414,8 +429,8 @@ __device__ __forceinline__ void process_piece(const SpmmArgs& a, bool active, u6
     const u32 p0 = ws;
     u32 c0 = 0, c1 = 0;
     float v0 = 0.0f, v1 = 0.0f;
-    if (p0 + lg < span) { c0 = ld_stream(colp + p0 + lg, pol_first); v0 = ld_stream(valp + p0 + lg, pol_first); }
-    if (p0 + G + lg < span) { c1 = ld_stream(colp + p0 + G + lg, pol_first); v1 = ld_stream(valp + p0 + G + lg, pol_first); }
+    if (p0 + lg < span) { SPMX_CHECK(j0 + p0 + lg < a.nnz, 0); c0 = ld_stream(colp + p0 + lg, pol_first); v0 = ld_stream(valp + p0 + lg, pol_first); }
+    if (p0 + G + lg < span) { SPMX_CHECK(j0 + p0 + G + lg < a.nnz, 0); c1 = ld_stream(colp + p0 + G + lg, pol_first); v1 = ld_stream(valp + p0 + G + lg, pol_first); }
 #if SPMX_PF_STREAM
     {  // the lines that hold positions [p0 + 2G, p0 + 2G + SPMX_PF_DIST): one line per lane and array
       const u32 q = p0 + 2 * G + 32 * (u32)lg;
@@ -430,6 +445,7 @@ __device__ __forceinline__ void process_piece(const SpmmArgs& a, bool active, u6
         const int li = qb + i * G + lg;
         eb[i] = 0;
         if (li < nw) {
+          SPMX_CHECK(wbase + li + 1 <= a.m, 2);
           const u64 hi = __ldg(a.row_ptr + wbase + li + 1);
           eb[i] = hi > j0 ? (u32)min(hi - j0, (u64)span) : 0u;
         }
@@ -442,6 +458,7 @@ __device__ __forceinline__ void process_piece(const SpmmArgs& a, bool active, u6
       for (int u = 0; u < U; ++u) {
         const u32 kq = __shfl_sync(kFullMask, c0, u, G);
         if (p0 + (u32)u < span) {
+          SPMX_CHECK((u64)kq < a.n_x, 3);
           const float* xr = xbase + (size_t)kq * (size_t)ldx;
 #pragma unroll
           for (int t = 0; t < NT; ++t)
@@ -480,6 +497,7 @@ __device__ __forceinline__ void process_piece(const SpmmArgs& a, bool active, u6
         const u32 s = lg == 0 ? prev_e : up;
         prev_e = __shfl_sync(kFullMask, e, G - 1, G);
         const unsigned ne = __ballot_sync(kFullMask, valid && e != s) & grp_mask;
+        SPMX_CHECK(!(valid && e != s) || count + __popc(ne & lt_mask) < W, 5);
         if (valid && e != s)
           s_rec[count + __popc(ne & lt_mask)] = make_uint2(e, wbase + li < r1 ? (u32)li : kCarryIdx);
         count += __popc(ne);
@@ -488,6 +506,7 @@ __device__ __forceinline__ void process_piece(const SpmmArgs& a, bool active, u6
         while (em) {
           const int src = (__ffs(em) - 1) - g * G;
           em &= em - 1;
+          SPMX_CHECK(wbase + q0 + src < a.m, 8);
           store_lane<D_CT, G, VEC, NT, RAGGED>(a, ywin + (size_t)(q0 + src) * (size_t)ldx, lg, acc, pol_first);
         }
       }
@@ -515,6 +534,7 @@ __device__ __forceinline__ void process_piece(const SpmmArgs& a, bool active, u6
       u32 c2 = 0;
       float v2 = 0.0f;
       if (nb + 2 * G + lg < L) {
+        SPMX_CHECK(j0 + p0 + nb + 2 * G + lg < a.nnz, 1);
         c2 = ld_stream(colp + p0 + nb + 2 * G + lg, pol_first);
         v2 = ld_stream(valp + p0 + nb + 2 * G + lg, pol_first);
       }
@@ -571,12 +591,14 @@ __device__ __forceinline__ void process_piece(const SpmmArgs& a, bool active, u6
         // the slot is free again: refill it before any row-end work (with four tiles per lane
         // the compiler turns this order into three branches per position: refill afterwards)
         if (kRefillFirst && t + U < rem) {
+          SPMX_CHECK((u64)kq < a.n_x, 4);
           const float* xr = xbase + (size_t)kq * (size_t)ldx;
 #pragma unroll
           for (int tt = 0; tt < NT; ++tt)
             if (tile_on<D_CT, G, VEC, RAGGED>(a, tt, lg)) xv[u][tt] = ld_x<VEC>(xr + tt * G * VEC, pol_last);
         }
         if (t == e_rel) {  // row k ends here: store it, start the next one
+          SPMX_CHECK(cur.y == kCarryIdx ? carry_lane != nullptr : wbase + cur.y < a.m, 7);
           float* dst = (cur.y != kCarryIdx) ? ywin + (size_t)cur.y * (size_t)ldx : carry_lane;
           store_lane<D_CT, G, VEC, NT, RAGGED>(a, dst, lg, acc, pol_first);
           zero_acc_from(acc, zero_f);
@@ -585,9 +607,11 @@ __device__ __forceinline__ void process_piece(const SpmmArgs& a, bool active, u6
           // (the copies are pinned inside the branch: the compiler otherwise hoists them in
           // front of every position's row-end test)
           asm volatile("mov.b32 %0, %2;\n\tmov.b32 %1, %3;" : "=r"(cur.x), "=r"(cur.y) : "r"(nxt.x), "r"(nxt.y));
+          SPMX_CHECK(k + 1 < W + 2, 6);
           nxt = s_rec[k + 1];
         }
         if (!kRefillFirst && t + U < rem) {
+          SPMX_CHECK((u64)kq < a.n_x, 4);
           const float* xr = xbase + (size_t)kq * (size_t)ldx;
 #pragma unroll
           for (int tt = 0; tt < NT; ++tt)
@@ -806,7 +830,7 @@ spmm_long_row_kernel(const SpmmArgs a, const LongRow* __restrict__ rows) {
       const u64 p = t * TP + i;
       cv_c[k] = 0;
       cv_v[k] = 0.0f;
-      if (i < TP && p < len) { cv_c[k] = __ldcs(colp + p); cv_v[k] = __ldcs(valp + p); }
+      if (i < TP && p < len) { SPMX_CHECK(lr.j0 + p < a.nnz, 9); cv_c[k] = __ldcs(colp + p); cv_v[k] = __ldcs(valp + p); }
     }
   };
   auto store_cv = [&](u64 t) {
@@ -825,13 +849,17 @@ spmm_long_row_kernel(const SpmmArgs a, const LongRow* __restrict__ rows) {
     const u64 left = t < n_tiles ? len - t * TP : 0;
     if (left >= (u64)TP && live == (1u << kLongK) - 1u) {  // a whole tile, every piece exists
 #pragma unroll
-      for (int k = 0; k < kLongK; ++k)
+      for (int k = 0; k < kLongK; ++k) {
+        SPMX_CHECK((u64)lds_u32(cs + cpos[k]) < a.n_x, 10);
         r[k] = ld_x<PIECE>(xcol[k] + (size_t)lds_u32(cs + cpos[k]) * (size_t)ldx, 0);
+      }
     } else {
 #pragma unroll
       for (int k = 0; k < kLongK; ++k)
-        if ((live >> k & 1u) && (u64)(cpos[k] >> 2) < left)
+        if ((live >> k & 1u) && (u64)(cpos[k] >> 2) < left) {
+          SPMX_CHECK((u64)lds_u32(cs + cpos[k]) < a.n_x, 10);
           r[k] = ld_x<PIECE>(xcol[k] + (size_t)lds_u32(cs + cpos[k]) * (size_t)ldx, 0);
+        }
     }
   };
   auto stash = [&](u64 t, const Piece (&r)[kLongK]) {  // a register set -> buffer t & 1
@@ -896,6 +924,7 @@ spmm_long_row_kernel(const SpmmArgs a, const LongRow* __restrict__ rows) {
     stash(t + 2, set0);
     __syncthreads();
   }
+  SPMX_CHECK(lr.row < a.m && lr.j1 <= a.nnz, 11);
   if (my_col < dw) __stcs(a.y + (size_t)lr.row * (size_t)ldx + a.c0 + my_col, acc);
 }
 

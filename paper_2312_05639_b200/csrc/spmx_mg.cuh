@@ -874,6 +874,7 @@ int spmx_mg_spmm(spmx_mg* mg, int steps, float* step_ms, float* ms_per_local_sha
           if (s.local_rank != lr) continue;
           const bool mark = step + 1 == steps;
           if (mark) CUDA_CHECK(cudaEventRecord(s.ev0, st));
+          s.plan->x_extra_rows = r.remapped ? r.n_hot : 0;
           run_kernels(r.ctx, s.plan, s.csr, r.x, d, s.y, st, 0, s.plan->n_chunks, nullptr);
           if (mark) CUDA_CHECK(cudaEventRecord(s.ev1, st));
         }

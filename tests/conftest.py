@@ -53,3 +53,21 @@ def ctx():
     c = Context.on_torch_stream(0)
     yield c
     c.close()
+
+
+def pytest_sessionfinish(session, exitstatus):
+    """tools/bounds_check.py runs the GPU suite against a library built with
+    -DSPMX_DEBUG_BOUNDS=1 and sets SPMX_BOUNDS_REPORT: the per-site counts of out-of-bounds
+    accesses the kernels would have made are written there (all zero = clean)."""
+    path = os.environ.get("SPMX_BOUNDS_REPORT")
+    if not path:
+        return
+    import ctypes as C
+    from paper_2312_05639_b200.binding import Lib
+    lib = Lib.get()
+    lib.lib.spmx_debug_bounds.argtypes = [C.POINTER(C.c_uint64)]
+    out = (C.c_uint64 * 16)()
+    rc = lib.lib.spmx_debug_bounds(out)
+    with open(path, "w") as f:
+        f.write(f"library {lib.path}\nrc {rc} launches {lib.launch_count()} pytest_exit {int(exitstatus)}\n")
+        f.write("violations per site: " + " ".join(str(int(v)) for v in out) + "\n")
