@@ -1,4 +1,4 @@
-"""Turns the files build/evidence_r02.sh leaves in gpurun_out/ into the tracked summaries under
+"""Turns the files tools/evidence_r02.sh leaves in gpurun_out/ into the tracked summaries under
 profiles/ and re-ties profiles/traffic.json to the kernel source that was profiled.
     python tools/update_profiles.py"""
 import hashlib
