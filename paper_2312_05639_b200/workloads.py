@@ -117,10 +117,17 @@ class Csr:
 
 def dense(rows: int, d: int, seed: int, dist: str = "uniform_pm1", device="cpu",
           stream: int = 7) -> torch.Tensor:
-    idx = torch.arange(rows * d, dtype=torch.int64, device=device)
-    h = hash_index(seed, stream, idx)
-    f = {"uniform_pm1": uniform_pm1, "normal": normal01}[dist](h)
-    return f.reshape(rows, d).contiguous()
+    # element i is a function of (seed, stream, i) alone: generated in blocks of 2^26 elements so
+    # that the int64 intermediates stay small (c5's X is 2^31 elements: 17 GB per int64 copy)
+    fn = {"uniform_pm1": uniform_pm1, "normal": normal01}[dist]
+    total = rows * d
+    out = torch.empty(total, dtype=torch.float32, device=device)
+    step = 1 << 26
+    for lo in range(0, total, step):
+        hi = min(lo + step, total)
+        idx = torch.arange(lo, hi, dtype=torch.int64, device=device)
+        out[lo:hi] = fn(hash_index(seed, stream, idx))
+    return out.reshape(rows, d)
 
 
 def _csr_from_sorted_keys(keys: torch.Tensor, m: int, n: int, shift: int, seed: int,
