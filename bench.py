@@ -372,6 +372,20 @@ def run_single(args):
            "api": "spmx_spmm_host (run_spmm with host buffers, pinned)"}
     # the e2e result must be the same Y as the device-resident path
     same = bool(np.array_equal(y_n.view(np.uint32), y.cpu().numpy().view(np.uint32)))
+    # The same call with PAGEABLE host arrays — what a caller of the reference's run_spmm holds
+    # (std::vector): staged through pinned slots by several host threads inside the library
+    # (csrc/spmx_stage.cuh). Informational; the contract's e2e above is from pinned memory.
+    pg = [np.array(v) for v in (rp_n, col_n, vals_n, x_n)]
+    y_pg = np.empty_like(y_n)
+    def e2e_pageable():
+        ectx.spmm_host(a.m, a.n, pg[0], pg[1], pg[2], pg[3], y=y_pg, strategy=args.strategy, flags=flags, nnz=a.nnz)
+    e2e_pageable()
+    t0 = time.perf_counter()
+    for _ in range(3):
+        e2e_pageable()
+    e2e["pageable_host_arrays"] = {"ms_per_step": (time.perf_counter() - t0) / 3 * 1e3, "steps": 3,
+                                   "matches_device_path": bool(np.array_equal(y_pg.view(np.uint32), y_n.view(np.uint32)))}
+    del pg, y_pg
 
     line = {"metric": METRIC, "value": gflops, "unit": UNIT, "n_gpus": 1, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True,

@@ -92,11 +92,17 @@ int spmx_ctx_destroy(spmx_ctx* ctx);
 int spmx_ctx_synchronize(spmx_ctx* ctx);
 int spmx_ctx_sm_count(spmx_ctx* ctx, int* out);
 
-/* raw device buffers on the context's device (X, Y and staging) */
+/* raw device buffers on the context's device (X, Y and staging).
+ * Host pointers of every entry point of this header may be pageable (std::vector, malloc — what
+ * the reference's CsrMatrix / DenseMatrix hold) or pinned. Pinned (or registered) memory goes to
+ * the copy engines directly and the copies are asynchronous on the context's stream. Pageable
+ * arrays of 1 MB and more are staged by the library's own host threads (several times the rate of
+ * the driver's staging): spmx_h2d then returns when the source has been read, spmx_d2h when the
+ * data has arrived — the contract cudaMemcpyAsync has for pageable memory. */
 int spmx_dev_alloc(spmx_ctx* ctx, size_t bytes, void** out);
 int spmx_dev_free(spmx_ctx* ctx, void* ptr);
-int spmx_h2d(spmx_ctx* ctx, void* dst_dev, const void* src_host, size_t bytes);  /* async on ctx stream */
-int spmx_d2h(spmx_ctx* ctx, void* dst_host, const void* src_dev, size_t bytes);  /* async on ctx stream */
+int spmx_h2d(spmx_ctx* ctx, void* dst_dev, const void* src_host, size_t bytes);  /* on the ctx stream */
+int spmx_d2h(spmx_ctx* ctx, void* dst_host, const void* src_dev, size_t bytes);  /* on the ctx stream */
 int spmx_host_alloc_pinned(size_t bytes, void** out);
 int spmx_host_free_pinned(void* ptr);
 

@@ -15,16 +15,19 @@
 #include <cstdlib>
 #include <cstring>
 #include <exception>
+#include <memory>
 #include <mutex>
 #include <new>
 #include <stdexcept>
 #include <string>
+#include <thread>
 #include <vector>
 
 #include "spmx_jit.cuh"
 #include "spmx_kernels.cuh"
 #include "spmx_partition.cuh"
 #include "spmx_probe.cuh"
+#include "spmx_stage.cuh"
 
 using spmx_dev::u64;
 
@@ -112,6 +115,8 @@ struct spmx_ctx {
   cudaStream_t s_aux = nullptr;  // long rows of exact-order plans run beside the main kernel (lazy)
   cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
   std::vector<cudaEvent_t> pipe_events;                // created once, reused by every call
+  // pageable host buffers are staged by several host threads (spmx_stage.cuh; lazy)
+  std::unique_ptr<spmx_stage::Stager> stage_up, stage_down;
   // grow-only staging used by spmx_spmm_host
   void* ws[5] = {nullptr, nullptr, nullptr, nullptr, nullptr};
   size_t ws_bytes[5] = {0, 0, 0, 0, 0};
@@ -849,6 +854,8 @@ int spmx_ctx_destroy(spmx_ctx* ctx) {
   return guarded([&] {
     check(ctx);
     cudaStreamSynchronize(ctx->stream);
+    ctx->stage_up.reset();
+    ctx->stage_down.reset();
     for (int i = 0; i < 5; ++i)
       if (ctx->ws[i]) cudaFree(ctx->ws[i]);
     cudaFree(ctx->d_err);
@@ -887,15 +894,63 @@ int spmx_dev_free(spmx_ctx* ctx, void* ptr) {
     CUDA_CHECK(cudaFree(ptr));
   });
 }
+namespace {
+
+// Worker threads for copies of pageable host memory (spmx_stage.cuh): half of the host's hardware
+// threads, at most 8 up and 6 down (measured on the 16-thread hosts of the B200 pool: c2 through
+// spmx_spmm_host from pageable arrays 52 -> 15.4 ms; more threads oversubscribe the memory bus).
+// SPMX_HOST_STAGE_THREADS = 0 leaves pageable copies to the driver.
+int stage_threads_up() {
+  const unsigned hw = std::max(4u, std::thread::hardware_concurrency());
+  return (int)env_u64("SPMX_HOST_STAGE_THREADS", std::min(8u, hw / 2));
+}
+int stage_threads_down() {
+  const unsigned hw = std::max(4u, std::thread::hardware_concurrency());
+  return (int)env_u64("SPMX_HOST_STAGE_THREADS_DOWN", std::min<u64>(std::min(6u, std::max(2u, hw / 2 - 2)),
+                                                                     (u64)std::max(1, stage_threads_up())));
+}
+constexpr size_t kStageMinBytes = 1u << 20;  // smaller copies are not worth a hand-over
+
+bool stage_this(const void* host, size_t bytes) {
+  return bytes >= kStageMinBytes && stage_threads_up() > 0 && spmx_stage::Stager::pageable(host);
+}
+spmx_stage::Stager& stager_up(spmx_ctx* ctx) {
+  if (!ctx->stage_up) ctx->stage_up = std::make_unique<spmx_stage::Stager>(ctx->device, stage_threads_up());
+  return *ctx->stage_up;
+}
+spmx_stage::Stager& stager_down(spmx_ctx* ctx) {
+  if (!ctx->stage_down) ctx->stage_down = std::make_unique<spmx_stage::Stager>(ctx->device, stage_threads_down());
+  return *ctx->stage_down;
+}
+
+// host -> device on `st`. Returns once the copy is enqueued (pinned source: asynchronous as
+// cudaMemcpyAsync is; pageable source: the source has been read when this returns, as with
+// cudaMemcpyAsync from pageable memory).
+void copy_h2d(spmx_ctx* ctx, void* dst, const void* src, size_t bytes, cudaStream_t st) {
+  if (bytes == 0) return;
+  if (stage_this(src, bytes)) {
+    spmx_stage::Stager::wait(stager_up(ctx).h2d(dst, src, bytes, st));
+    return;
+  }
+  CUDA_CHECK(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyHostToDevice, st));
+}
+// device -> host on `st`; with a pageable destination the data has arrived when this returns
+void copy_d2h(spmx_ctx* ctx, void* dst, const void* src, size_t bytes, cudaStream_t st) {
+  if (bytes == 0) return;
+  if (stage_this(dst, bytes)) {
+    spmx_stage::Stager::wait(stager_down(ctx).d2h(dst, src, bytes, st));
+    return;
+  }
+  CUDA_CHECK(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyDeviceToHost, st));
+}
+
+}  // namespace
+
 int spmx_h2d(spmx_ctx* ctx, void* dst, const void* src, size_t bytes) {
-  return guarded([&] {
-    CUDA_CHECK(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyHostToDevice, check(ctx)->stream));
-  });
+  return guarded([&] { copy_h2d(check(ctx), dst, src, bytes, ctx->stream); });
 }
 int spmx_d2h(spmx_ctx* ctx, void* dst, const void* src, size_t bytes) {
-  return guarded([&] {
-    CUDA_CHECK(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyDeviceToHost, check(ctx)->stream));
-  });
+  return guarded([&] { copy_d2h(check(ctx), dst, src, bytes, ctx->stream); });
 }
 int spmx_host_alloc_pinned(size_t bytes, void** out) {
   return guarded([&] { CUDA_CHECK(cudaMallocHost(out, bytes ? bytes : 1)); });
@@ -921,14 +976,9 @@ int spmx_csr_upload(spmx_ctx* ctx, int64_t m, int64_t n, int64_t nnz, const uint
       a->row_ptr = dev_alloc<u64>((size_t)m + 1);
       a->col = dev_alloc<uint32_t>((size_t)nnz);
       a->vals = dev_alloc<float>((size_t)nnz);
-      CUDA_CHECK(cudaMemcpyAsync(a->row_ptr, row_ptr, ((size_t)m + 1) * 8, cudaMemcpyHostToDevice,
-                                 ctx->stream));
-      if (nnz) {
-        CUDA_CHECK(cudaMemcpyAsync(a->col, col, (size_t)nnz * 4, cudaMemcpyHostToDevice,
-                                   ctx->stream));
-        CUDA_CHECK(cudaMemcpyAsync(a->vals, vals, (size_t)nnz * 4, cudaMemcpyHostToDevice,
-                                   ctx->stream));
-      }
+      copy_h2d(ctx, a->row_ptr, row_ptr, ((size_t)m + 1) * 8, ctx->stream);
+      copy_h2d(ctx, a->col, col, (size_t)nnz * 4, ctx->stream);
+      copy_h2d(ctx, a->vals, vals, (size_t)nnz * 4, ctx->stream);
       validate_on_device(ctx, a);
     } catch (...) {
       spmx_csr_destroy(a);
@@ -1202,6 +1252,31 @@ int spmx_spmm_host(spmx_ctx* ctx, int64_t m, int64_t n, int64_t nnz, const uint6
       CUDA_CHECK(cudaStreamCreateWithFlags(&ctx->s_x, cudaStreamNonBlocking));
     }
     cudaStream_t s0 = ctx->stream, s1 = ctx->s_compute, s2 = ctx->s_d2h, s3 = ctx->s_x;
+    // Pageable host arrays (what a caller of the reference's run_spmm holds: std::vector) are
+    // staged through pinned slots by several host threads instead of the driver's single one
+    // (spmx_stage.cuh); pinned or registered arrays go to the copy engines directly.
+    using spmx_stage::Stager;
+    auto staged = [&](const void* p, size_t bytes) { return stage_this(p, bytes); };
+    const size_t x_bytes = (size_t)n * (size_t)d * 4, y_bytes = (size_t)m * (size_t)d * 4;
+    const bool st_rp = staged(row_ptr, ((size_t)m + 1) * 8), st_x = staged(x, x_bytes);
+    const bool st_col = staged(col, (size_t)nnz * 4), st_val = staged(vals, (size_t)nnz * 4);
+    const bool st_y = staged(y, y_bytes);
+    if (st_rp || st_x || st_col || st_val) stager_up(ctx);
+    if (st_y) stager_down(ctx);
+    std::vector<Stager::Ticket> pending;  // staged copies not yet waited for
+    auto drain_quiet = [&]() noexcept {
+      for (auto& t : pending) Stager::wait_quiet(t);
+      pending.clear();
+    };
+    auto up = [&](void* dst, const void* src, size_t bytes, bool stage, cudaStream_t st) -> Stager::Ticket {
+      if (bytes == 0) return nullptr;
+      if (stage) {
+        pending.push_back(ctx->stage_up->h2d(dst, src, bytes, st));
+        return pending.back();
+      }
+      CUDA_CHECK(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyHostToDevice, st));
+      return nullptr;
+    };
     constexpr int kMaxBlocks = 32;
     cudaEvent_t ev_t[4];            // timing marks on stream 0 / 2
     cudaEvent_t ev_x, ev_in[kMaxBlocks], ev_done[kMaxBlocks];
@@ -1239,11 +1314,11 @@ int spmx_spmm_host(spmx_ctx* ctx, int64_t m, int64_t n, int64_t nnz, const uint6
       for (int b = 0; b < kMaxBlocks; ++b) { mk(ev_in[b], false); mk(ev_done[b], false); }
       const auto t_host0 = std::chrono::steady_clock::now();
       CUDA_CHECK(cudaEventRecord(ev_t[0], s0));
-      CUDA_CHECK(cudaMemcpyAsync(d_rp, row_ptr, ((size_t)m + 1) * 8, cudaMemcpyHostToDevice, s0));
+      Stager::wait(up(d_rp, row_ptr, ((size_t)m + 1) * 8, st_rp, s0));  // enqueued: stream 0 orders the rest
       // X moves on its own stream while the plan is being built from row_ptr
       CUDA_CHECK(cudaStreamWaitEvent(s3, ev_t[0], 0));
-      CUDA_CHECK(cudaMemcpyAsync(d_x, x, (size_t)n * (size_t)d * 4, cudaMemcpyHostToDevice, s3));
-      CUDA_CHECK(cudaEventRecord(ev_x, s3));
+      Stager::Ticket x_ticket = up(d_x, x, x_bytes, st_x, s3);
+      if (!x_ticket) CUDA_CHECK(cudaEventRecord(ev_x, s3));
       CUDA_CHECK(cudaMemsetAsync(ctx->d_err, 0, sizeof(int), s0));
       spmx_dev::validate_row_ptr_kernel<<<validate_grid(ctx, (u64)m), 256, 0, s0>>>(
           d_rp, (u64)m, (u64)nnz, ctx->d_err);
@@ -1279,6 +1354,10 @@ int spmx_spmm_host(spmx_ctx* ctx, int64_t m, int64_t n, int64_t nnz, const uint6
         // a block's first chunk may start inside a row whose head is in the previous block; the
         // nonzeros it needs still start at its own chunk_nnz, which is what nnz_b holds
       }
+      if (x_ticket) {  // staged X: every piece has to be on stream 3 before the event that marks its end
+        Stager::wait(x_ticket);
+        CUDA_CHECK(cudaEventRecord(ev_x, s3));
+      }
       CUDA_CHECK(cudaStreamWaitEvent(s0, ev_x, 0));
       CUDA_CHECK(cudaEventRecord(ev_t[1], s0));
       // The blocks go LAST TO FIRST: on a power-law matrix the last block (equal merge items)
@@ -1291,8 +1370,10 @@ int spmx_spmm_host(spmx_ctx* ctx, int64_t m, int64_t n, int64_t nnz, const uint6
         const int b = nblocks - 1 - bi;
         const u64 n0 = nnz_b[b], n1 = nnz_b[b + 1];
         if (n1 > n0) {
-          CUDA_CHECK(cudaMemcpyAsync(d_col + n0, col + n0, (n1 - n0) * 4, cudaMemcpyHostToDevice, s0));
-          CUDA_CHECK(cudaMemcpyAsync(d_vals + n0, vals + n0, (n1 - n0) * 4, cudaMemcpyHostToDevice, s0));
+          Stager::Ticket tc = up(d_col + n0, col + n0, (n1 - n0) * 4, st_col, s0);
+          Stager::Ticket tv = up(d_vals + n0, vals + n0, (n1 - n0) * 4, st_val, s0);
+          Stager::wait(tc);
+          Stager::wait(tv);
         }
         CUDA_CHECK(cudaEventRecord(ev_in[b], s0));
         CUDA_CHECK(cudaStreamWaitEvent(s1, ev_in[b], 0));
@@ -1307,9 +1388,14 @@ int spmx_spmm_host(spmx_ctx* ctx, int64_t m, int64_t n, int64_t nnz, const uint6
         CUDA_CHECK(cudaStreamWaitEvent(s2, ev_done[b], 0));
         const u64 r0 = row_b[b], r1 = (b + 1 == nblocks) ? (u64)m : row_b[b + 1];
         if (bi == 0) CUDA_CHECK(cudaEventRecord(ev_t[2], s2));
-        if (r1 > r0)
-          CUDA_CHECK(cudaMemcpyAsync(y + r0 * (size_t)d, d_y + r0 * (size_t)d, (r1 - r0) * (size_t)d * 4,
-                                     cudaMemcpyDeviceToHost, s2));
+        if (r1 > r0) {
+          if (st_y)  // done when the rows are in the caller's array (waited for below)
+            pending.push_back(ctx->stage_down->d2h(y + r0 * (size_t)d, d_y + r0 * (size_t)d,
+                                                   (r1 - r0) * (size_t)d * 4, s2));
+          else
+            CUDA_CHECK(cudaMemcpyAsync(y + r0 * (size_t)d, d_y + r0 * (size_t)d, (r1 - r0) * (size_t)d * 4,
+                                       cudaMemcpyDeviceToHost, s2));
+        }
       }
       if (nblocks > 1 && plan->may_carry) {
         // deferred chains: those closed in block b whose first partial is in an earlier block
@@ -1318,6 +1404,10 @@ int spmx_spmm_host(spmx_ctx* ctx, int64_t m, int64_t n, int64_t nnz, const uint6
                       /*fixup_only=*/true);
         CUDA_CHECK(cudaEventRecord(ev_done[0], s1));
         CUDA_CHECK(cudaStreamWaitEvent(s2, ev_done[0], 0));
+        // staged downloads write the caller's array from worker threads: the rows downloaded
+        // again below must land after the block copies that hold their earlier values
+        for (auto& t : pending) Stager::wait(t);
+        pending.clear();
         for (int b = 1; b < nblocks; ++b) {
           const u64 r = row_b[b];  // the row block b starts in
           if (r < (u64)m)
@@ -1325,6 +1415,8 @@ int spmx_spmm_host(spmx_ctx* ctx, int64_t m, int64_t n, int64_t nnz, const uint6
                                        cudaMemcpyDeviceToHost, s2));
         }
       }
+      for (auto& t : pending) Stager::wait(t);
+      pending.clear();
       CUDA_CHECK(cudaEventRecord(ev_t[3], s2));
       CUDA_CHECK(cudaMemcpyAsync(&err, ctx->d_err, sizeof(int), cudaMemcpyDeviceToHost, s2));
       CUDA_CHECK(cudaStreamSynchronize(s2));
@@ -1346,6 +1438,7 @@ int spmx_spmm_host(spmx_ctx* ctx, int64_t m, int64_t n, int64_t nnz, const uint6
         times_ms[5] = (double)nblocks;
       }
     } catch (...) {
+      drain_quiet();  // workers still read the caller's arrays / write Y
       cudaStreamSynchronize(s0);
       cudaStreamSynchronize(s1);
       cudaStreamSynchronize(s2);

@@ -666,8 +666,7 @@ int spmx_mg_shard_host(spmx_mg* mg, int64_t m, int64_t n, int64_t nnz, const uin
       CUDA_CHECK(cudaSetDevice(r0.device));
       u64* d_rp = dev_alloc<u64>((size_t)m + 1);
       try {
-        CUDA_CHECK(cudaMemcpyAsync(d_rp, row_ptr, ((size_t)m + 1) * 8, cudaMemcpyHostToDevice,
-                                   r0.ctx->stream));
+        copy_h2d(r0.ctx, d_rp, row_ptr, ((size_t)m + 1) * 8, r0.ctx->stream);
         mg_split(mg, r0.ctx, d_rp, shard_by);
       } catch (...) {
         cudaFree(d_rp);
@@ -678,8 +677,7 @@ int spmx_mg_shard_host(spmx_mg* mg, int64_t m, int64_t n, int64_t nnz, const uin
         const MgRank& r = mg->ranks[(size_t)lr];
         const void* src = what == 0 ? (const void*)(row_ptr + first)
                         : what == 1 ? (const void*)(col + first) : (const void*)(vals + first);
-        CUDA_CHECK(cudaMemcpyAsync(dst, src, count * (what == 0 ? 8 : 4), cudaMemcpyHostToDevice,
-                                   r.ctx->stream));
+        copy_h2d(r.ctx, dst, src, count * (what == 0 ? 8 : 4), r.ctx->stream);  // pageable arrays: staged by host threads
       };
       // the split has validated row_ptr, so these reads stay inside [0, nnz]
       mg_place(mg, fetch, [&](u64 r) { return (u64)row_ptr[r]; });
@@ -785,8 +783,7 @@ int spmx_mg_broadcast_x_host(spmx_mg* mg, const float* x_host, int root_rank, in
       if (!x_host && x_rows > 0) throw InvalidArg("run_spmm: null X on the root rank");
       CUDA_CHECK(cudaSetDevice(r.device));
       CUDA_CHECK(cudaEventRecord(r.ev0, r.ctx->stream));
-      CUDA_CHECK(cudaMemcpyAsync(r.x, x_host, (size_t)x_rows * (size_t)d * 4, cudaMemcpyHostToDevice,
-                                 r.ctx->stream));
+      copy_h2d(r.ctx, r.x, x_host, (size_t)x_rows * (size_t)d * 4, r.ctx->stream);
       CUDA_CHECK(cudaEventRecord(r.ev1, r.ctx->stream));
       CUDA_CHECK(cudaEventSynchronize(r.ev1));
       if (h2d_ms) CUDA_CHECK(cudaEventElapsedTime(h2d_ms, r.ev0, r.ev1));
@@ -907,19 +904,26 @@ int spmx_mg_download_y(spmx_mg* mg, float* y_host) {
     check(mg);
     if (!y_host && mg->m > 0) throw InvalidArg("spmx_mg_download_y: null Y");
     const size_t d = (size_t)mg->d;
+    std::vector<spmx_stage::Stager::Ticket> tickets;
+    for (MgShard& s : mg->shards)  // checked before the first copy: staged copies run on worker threads
+      if (!s.y) throw LogicErr("spmx_mg_download_y: spmx_mg_spmm has not run");
     for (MgShard& s : mg->shards) {
       MgRank& r = mg->ranks[(size_t)s.local_rank];
-      if (!s.y) throw LogicErr("spmx_mg_download_y: spmx_mg_spmm has not run");
       CUDA_CHECK(cudaSetDevice(r.device));
       const size_t rows = (size_t)(s.row_end - s.row_begin);
-      if (rows)
-        CUDA_CHECK(cudaMemcpyAsync(y_host + (size_t)s.row_begin * d, s.y, rows * d * 4,
-                                   cudaMemcpyDeviceToHost, r.ctx->stream));
+      if (!rows) continue;
+      float* dst = y_host + (size_t)s.row_begin * d;
+      if (stage_this(dst, rows * d * 4))  // pageable Y: the shards of all GPUs are staged side by side
+        tickets.push_back(stager_down(r.ctx).d2h(dst, s.y, rows * d * 4, r.ctx->stream));
+      else
+        CUDA_CHECK(cudaMemcpyAsync(dst, s.y, rows * d * 4, cudaMemcpyDeviceToHost, r.ctx->stream));
     }
+    for (auto& t : tickets) spmx_stage::Stager::wait_quiet(t);
     for (MgRank& r : mg->ranks) {
       CUDA_CHECK(cudaSetDevice(r.device));
       CUDA_CHECK(cudaStreamSynchronize(r.ctx->stream));
     }
+    for (auto& t : tickets) spmx_stage::Stager::wait(t);  // rethrows a worker's error
   });
 }
 
@@ -928,21 +932,30 @@ int spmx_mg_download_y_shards(spmx_mg* mg, float* const* host_per_local_shard) {
     check(mg);
     if (!host_per_local_shard && !mg->shards.empty()) throw InvalidArg("spmx_mg_download_y_shards: null list");
     const size_t d = (size_t)mg->d;
+    std::vector<spmx_stage::Stager::Ticket> tickets;
+    for (size_t i = 0; i < mg->shards.size(); ++i) {  // checked before the first copy
+      if (!mg->shards[i].y) throw LogicErr("spmx_mg_download_y_shards: spmx_mg_spmm has not run");
+      if (mg->shards[i].row_end > mg->shards[i].row_begin && !host_per_local_shard[i])
+        throw InvalidArg("spmx_mg_download_y_shards: null Y block");
+    }
     for (size_t i = 0; i < mg->shards.size(); ++i) {
       MgShard& s = mg->shards[i];
       MgRank& r = mg->ranks[(size_t)s.local_rank];
-      if (!s.y) throw LogicErr("spmx_mg_download_y_shards: spmx_mg_spmm has not run");
       const size_t rows = (size_t)(s.row_end - s.row_begin);
       if (!rows) continue;
-      if (!host_per_local_shard[i]) throw InvalidArg("spmx_mg_download_y_shards: null Y block");
       CUDA_CHECK(cudaSetDevice(r.device));
-      CUDA_CHECK(cudaMemcpyAsync(host_per_local_shard[i], s.y, rows * d * 4, cudaMemcpyDeviceToHost,
-                                 r.ctx->stream));
+      if (stage_this(host_per_local_shard[i], rows * d * 4))
+        tickets.push_back(stager_down(r.ctx).d2h(host_per_local_shard[i], s.y, rows * d * 4, r.ctx->stream));
+      else
+        CUDA_CHECK(cudaMemcpyAsync(host_per_local_shard[i], s.y, rows * d * 4, cudaMemcpyDeviceToHost,
+                                   r.ctx->stream));
     }
+    for (auto& t : tickets) spmx_stage::Stager::wait_quiet(t);
     for (MgRank& r : mg->ranks) {
       CUDA_CHECK(cudaSetDevice(r.device));
       CUDA_CHECK(cudaStreamSynchronize(r.ctx->stream));
     }
+    for (auto& t : tickets) spmx_stage::Stager::wait(t);
   });
 }
 

@@ -52,3 +52,16 @@ def test_product_never_imports_the_oracle():
                 text = open(os.path.join(dirpath, f), errors="replace").read()
                 hits = [b for b in banned if b in text]
                 assert not hits, (f, hits)
+
+
+def test_stream_copy_equals_memcpy(tmp_path):
+    """csrc/spmx_stage.cuh: the non-temporal copy that stages pageable host arrays, every size and
+    alignment against memcpy (host-only: compiled with g++, no device call)."""
+    import subprocess
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    exe = str(tmp_path / "test_stream_copy")
+    subprocess.check_call(["g++", "-std=c++17", "-O2", "-Wall", "-I/usr/local/cuda/include", "-o", exe,
+                           os.path.join(root, "tests", "host", "test_stream_copy.cpp"), "-lpthread"])
+    out = subprocess.run([exe], capture_output=True, text=True)
+    assert out.returncode == 0, out.stdout + out.stderr
+    assert "stream_copy ok" in out.stdout
