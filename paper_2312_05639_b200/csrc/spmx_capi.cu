@@ -115,8 +115,6 @@ struct spmx_ctx {
   cudaStream_t s_aux = nullptr;  // long rows of exact-order plans run beside the main kernel (lazy)
   cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
   std::vector<cudaEvent_t> pipe_events;                // created once, reused by every call
-  // pageable host buffers are staged by several host threads (spmx_stage.cuh; lazy)
-  std::unique_ptr<spmx_stage::Stager> stage_up, stage_down;
   // grow-only staging used by spmx_spmm_host
   void* ws[5] = {nullptr, nullptr, nullptr, nullptr, nullptr};
   size_t ws_bytes[5] = {0, 0, 0, 0, 0};
@@ -854,8 +852,6 @@ int spmx_ctx_destroy(spmx_ctx* ctx) {
   return guarded([&] {
     check(ctx);
     cudaStreamSynchronize(ctx->stream);
-    ctx->stage_up.reset();
-    ctx->stage_down.reset();
     for (int i = 0; i < 5; ++i)
       if (ctx->ws[i]) cudaFree(ctx->ws[i]);
     cudaFree(ctx->d_err);
@@ -915,12 +911,10 @@ bool stage_this(const void* host, size_t bytes) {
   return bytes >= kStageMinBytes && stage_threads_up() > 0 && spmx_stage::Stager::pageable(host);
 }
 spmx_stage::Stager& stager_up(spmx_ctx* ctx) {
-  if (!ctx->stage_up) ctx->stage_up = std::make_unique<spmx_stage::Stager>(ctx->device, stage_threads_up());
-  return *ctx->stage_up;
+  return spmx_stage::shared_stager(ctx->device, true, stage_threads_up());
 }
 spmx_stage::Stager& stager_down(spmx_ctx* ctx) {
-  if (!ctx->stage_down) ctx->stage_down = std::make_unique<spmx_stage::Stager>(ctx->device, stage_threads_down());
-  return *ctx->stage_down;
+  return spmx_stage::shared_stager(ctx->device, false, stage_threads_down());
 }
 
 // host -> device on `st`. Returns once the copy is enqueued (pinned source: asynchronous as
@@ -1261,8 +1255,6 @@ int spmx_spmm_host(spmx_ctx* ctx, int64_t m, int64_t n, int64_t nnz, const uint6
     const bool st_rp = staged(row_ptr, ((size_t)m + 1) * 8), st_x = staged(x, x_bytes);
     const bool st_col = staged(col, (size_t)nnz * 4), st_val = staged(vals, (size_t)nnz * 4);
     const bool st_y = staged(y, y_bytes);
-    if (st_rp || st_x || st_col || st_val) stager_up(ctx);
-    if (st_y) stager_down(ctx);
     std::vector<Stager::Ticket> pending;  // staged copies not yet waited for
     auto drain_quiet = [&]() noexcept {
       for (auto& t : pending) Stager::wait_quiet(t);
@@ -1271,7 +1263,7 @@ int spmx_spmm_host(spmx_ctx* ctx, int64_t m, int64_t n, int64_t nnz, const uint6
     auto up = [&](void* dst, const void* src, size_t bytes, bool stage, cudaStream_t st) -> Stager::Ticket {
       if (bytes == 0) return nullptr;
       if (stage) {
-        pending.push_back(ctx->stage_up->h2d(dst, src, bytes, st));
+        pending.push_back(stager_up(ctx).h2d(dst, src, bytes, st));
         return pending.back();
       }
       CUDA_CHECK(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyHostToDevice, st));
@@ -1390,7 +1382,7 @@ int spmx_spmm_host(spmx_ctx* ctx, int64_t m, int64_t n, int64_t nnz, const uint6
         if (bi == 0) CUDA_CHECK(cudaEventRecord(ev_t[2], s2));
         if (r1 > r0) {
           if (st_y)  // done when the rows are in the caller's array (waited for below)
-            pending.push_back(ctx->stage_down->d2h(y + r0 * (size_t)d, d_y + r0 * (size_t)d,
+            pending.push_back(stager_down(ctx).d2h(y + r0 * (size_t)d, d_y + r0 * (size_t)d,
                                                    (r1 - r0) * (size_t)d * 4, s2));
           else
             CUDA_CHECK(cudaMemcpyAsync(y + r0 * (size_t)d, d_y + r0 * (size_t)d, (r1 - r0) * (size_t)d * 4,

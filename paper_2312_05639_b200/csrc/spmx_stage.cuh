@@ -95,17 +95,11 @@ class Stager {
 
   Stager(int device, int workers) : device_(device) {
     if (workers < 1) workers = 1;
+    // slots and events are created by their worker on its first piece (pinned allocations are
+    // slow: a copy of a few pieces should not pay for every worker's slots)
     slots_.resize((size_t)workers * 2, nullptr);
     events_.resize((size_t)workers * 2, nullptr);
     busy_.assign((size_t)workers * 2, 0);
-    for (size_t i = 0; i < slots_.size(); ++i) {
-      if (cudaMallocHost(&slots_[i], kPiece) != cudaSuccess ||
-          cudaEventCreateWithFlags(&events_[i], cudaEventDisableTiming) != cudaSuccess) {
-        cudaGetLastError();
-        release();
-        throw std::runtime_error("host stager: cannot allocate pinned staging slots");
-      }
-    }
     for (int w = 0; w < workers; ++w) threads_.emplace_back([this, w] { run(w); });
   }
   ~Stager() {
@@ -183,12 +177,21 @@ class Stager {
         if (e != cudaSuccess && err.empty()) err = std::string("host stager: ") + what + ": " + cudaGetErrorString(e);
         return e == cudaSuccess;
       };
+      if (!slots_[slot]) {
+        if (!ok(cudaMallocHost(&slots_[slot], kPiece), "pinned slot") ||
+            !ok(cudaEventCreateWithFlags(&events_[slot], cudaEventDisableTiming), "slot event")) {
+          if (slots_[slot] && !events_[slot]) { cudaFreeHost(slots_[slot]); slots_[slot] = nullptr; }
+          cudaGetLastError();
+        }
+      }
       // the slot's previous DMA (an upload enqueued two pieces ago) must have read it
       if (busy_[slot]) {
         ok(cudaEventSynchronize(events_[slot]), "slot wait");
         busy_[slot] = 0;
       }
-      if (p.up) {
+      if (!err.empty()) {
+        // no slot: fall through to the completion below with the error recorded
+      } else if (p.up) {
         stream_copy(slots_[slot], p.src, p.bytes);
         if (ok(cudaMemcpyAsync(p.dst, slots_[slot], p.bytes, cudaMemcpyHostToDevice, p.stream), "H2D") &&
             ok(cudaEventRecord(events_[slot], p.stream), "event"))
@@ -227,5 +230,18 @@ class Stager {
   std::deque<Piece> queue_;
   bool stop_ = false;
 };
+
+// One stager per device and direction for the whole process, shared by every context (its jobs
+// are independent of each other) and never destroyed: worker threads and pinned slots outlive
+// the contexts, and nothing of the CUDA runtime is torn down from a static destructor at exit.
+inline Stager& shared_stager(int device, bool up, int workers) {
+  static std::mutex mu;
+  static std::vector<Stager*> inst;  // [2 * device + up]
+  std::lock_guard<std::mutex> lk(mu);
+  const size_t key = (size_t)device * 2 + (up ? 1 : 0);
+  if (inst.size() <= key) inst.resize(key + 1, nullptr);
+  if (!inst[key]) inst[key] = new Stager(device, workers);
+  return *inst[key];
+}
 
 }  // namespace spmx_stage
