@@ -167,6 +167,11 @@ struct MgRank {  // one GPU driven by this process
   bool window = false;
   cudaEvent_t ev0 = nullptr, ev1 = nullptr;
   float ms = 0.f;
+  size_t hot_cap = 0, slot_n = 0;  // element counts of hot_cols / slot_of
+  // Device buffers of the shards that were last released, kept for the next sharding: a caller
+  // that shards the same matrix again (every end-to-end call does) asks for exactly these sizes,
+  // and cudaMalloc / cudaFree of gigabyte buffers cost 50 - 500 ms per call with a large spread.
+  std::vector<std::pair<void*, size_t>> spare;
 };
 
 struct MgShard {
@@ -237,14 +242,45 @@ void for_each_rank(spmx_mg* g, F&& f) {
     if (e) std::rethrow_exception(e);
 }
 
+// (the rank's device is current)
+void mg_drop_spare(MgRank& r) {
+  for (auto& e : r.spare) cudaFree(e.first);
+  r.spare.clear();
+}
+template <typename T>
+T* mg_take(MgRank& r, size_t count) {
+  const size_t bytes = (count ? count : 1) * sizeof(T);
+  for (size_t i = 0; i < r.spare.size(); ++i)
+    if (r.spare[i].second == bytes) {
+      T* p = (T*)r.spare[i].first;
+      r.spare.erase(r.spare.begin() + (long)i);
+      return p;
+    }
+  mg_drop_spare(r);  // other sizes: another matrix, the old buffers are of no use
+  T* p = nullptr;
+  CUDA_CHECK(cudaMalloc(&p, bytes));
+  return p;
+}
+template <typename T>
+void mg_give(MgRank& r, T* p, size_t count) {
+  if (!p) return;
+  if (r.spare.size() >= 64) { cudaFree(p); return; }
+  r.spare.emplace_back((void*)p, (count ? count : 1) * sizeof(T));
+}
+
 void mg_free_shards(spmx_mg* g) {
   for (MgShard& s : g->shards) {
     MgRank& r = g->ranks[s.local_rank];
     cudaSetDevice(r.device);
     cudaStreamSynchronize(r.ctx->stream);
     if (s.plan) plan_free(s.plan);
-    if (s.csr) spmx_csr_destroy(s.csr);
-    if (s.y) cudaFree(s.y);
+    if (s.csr) {  // the arrays belong to the driver (owned = false): kept for the next sharding
+      mg_give(r, s.csr->row_ptr, (size_t)s.csr->m + 1);
+      mg_give(r, s.csr->col, (size_t)s.csr->nnz);
+      mg_give(r, s.csr->vals, (size_t)s.csr->nnz);
+      spmx_csr_destroy(s.csr);
+    }
+    mg_give(r, s.y, s.y_floats);
     if (s.ev0) cudaEventDestroy(s.ev0);
     if (s.ev1) cudaEventDestroy(s.ev1);
   }
@@ -253,9 +289,10 @@ void mg_free_shards(spmx_mg* g) {
   for (MgRank& r : g->ranks) {  // the hot-row tables describe the shards that just went away
     if (!r.ctx) continue;
     cudaSetDevice(r.device);
-    if (r.hot_cols) cudaFree(r.hot_cols);
-    if (r.slot_of) cudaFree(r.slot_of);
+    mg_give(r, r.hot_cols, r.hot_cap);
+    mg_give(r, r.slot_of, r.slot_n);
     r.hot_cols = r.slot_of = nullptr;
+    r.hot_cap = r.slot_n = 0;
     r.n_hot = 0;
     r.remapped = false;
   }
@@ -268,6 +305,7 @@ void mg_free(spmx_mg* g) {
   for (MgRank& r : g->ranks) {
     if (!r.ctx) continue;  // creation failed before anything was allocated on this device
     cudaSetDevice(r.device);
+    mg_drop_spare(r);
     cudaStreamSynchronize(r.ctx->stream);
     if (r.comm && nc.CommDestroy) nc.CommDestroy(r.comm);
     if (r.x && r.x_owned) cudaFree(r.x);
@@ -330,13 +368,13 @@ void mg_place(spmx_mg* g, Fetch&& fetch, NnzAt&& nnz_at) {
     a->m = (int64_t)rows;
     a->n = g->n;
     a->nnz = (int64_t)s.nnz;
-    a->owned = true;
+    a->owned = false;  // the arrays go back to the rank's spare list (mg_free_shards)
     s.csr = a;
     g->shards.push_back(s);  // from here on mg_free_shards releases it
     MgShard& t = g->shards.back();
-    a->row_ptr = dev_alloc<u64>((size_t)rows + 1);
-    a->col = dev_alloc<uint32_t>((size_t)s.nnz);
-    a->vals = dev_alloc<float>((size_t)s.nnz);
+    a->row_ptr = mg_take<u64>(r, (size_t)rows + 1);
+    a->col = mg_take<uint32_t>(r, (size_t)s.nnz);
+    a->vals = mg_take<float>(r, (size_t)s.nnz);
     CUDA_CHECK(cudaEventCreate(&t.ev0));
     CUDA_CHECK(cudaEventCreate(&t.ev1));
     fetch((void*)a->row_ptr, 0, s.row_begin, rows + 1, lr);
@@ -422,8 +460,10 @@ void mg_build_hot(spmx_mg* g) {
     CUDA_CHECK(cudaSetDevice(r.device));
     cudaStream_t st = r.ctx->stream;
     const u64 n = (u64)g->n;
-    r.slot_of = dev_alloc<uint32_t>((size_t)n);
-    r.hot_cols = dev_alloc<uint32_t>((size_t)cap);
+    r.slot_of = mg_take<uint32_t>(r, (size_t)n);
+    r.slot_n = (size_t)n;
+    r.hot_cols = mg_take<uint32_t>(r, (size_t)cap);
+    r.hot_cap = (size_t)cap;
     CUDA_CHECK(cudaMemsetAsync(r.slot_of, 0, (size_t)n * 4, st));
     for (const MgShard& s : g->shards)
       if (s.local_rank == (int)lr && s.nnz) {
@@ -853,10 +893,12 @@ int spmx_mg_spmm(spmx_mg* mg, int steps, float* step_ms, float* ms_per_local_sha
       if (!s.plan) throw LogicErr("spmx_mg_spmm: spmx_mg_plan has not been called");
       const size_t need = (size_t)(s.row_end - s.row_begin) * (size_t)d;
       if (s.y_floats < need) {
-        CUDA_CHECK(cudaSetDevice(mg->ranks[(size_t)s.local_rank].device));
+        MgRank& ry = mg->ranks[(size_t)s.local_rank];
+        CUDA_CHECK(cudaSetDevice(ry.device));
         if (s.y) CUDA_CHECK(cudaFree(s.y));
         s.y = nullptr;
-        s.y = dev_alloc<float>(need);
+        s.y_floats = 0;
+        s.y = mg_take<float>(ry, need);
         s.y_floats = need;
       }
     }
