@@ -65,3 +65,25 @@ def test_stream_copy_equals_memcpy(tmp_path):
     out = subprocess.run([exe], capture_output=True, text=True)
     assert out.returncode == 0, out.stdout + out.stderr
     assert "stream_copy ok" in out.stdout
+
+
+def _build_c_example(tmp_path):
+    import subprocess
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    pkg = os.path.join(root, "paper_2312_05639_b200")
+    exe = str(tmp_path / "spmx_minimal")
+    subprocess.check_call(["gcc", "-std=c99", "-Wall", "-Wextra", "-pedantic", "-Werror", "-o", exe,
+                           os.path.join(root, "examples", "spmx_minimal.c"), "-L" + pkg, "-lspmx_b200",
+                           "-Wl,-rpath," + pkg])
+    return exe
+
+
+def test_header_is_plain_c_and_links_from_c(tmp_path):
+    """include/spmx_b200.h is the C-ABI boundary: it must compile as pedantic C99 (no C++ types in
+    any signature) and a C program must link against the library (no compute call here)."""
+    import subprocess
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    subprocess.check_call(["gcc", "-std=c99", "-Wall", "-Wextra", "-pedantic", "-Werror", "-fsyntax-only", "-x", "c",
+                           os.path.join(root, "include", "spmx_b200.h")])
+    out = subprocess.run([_build_c_example(tmp_path), "--link-only"], capture_output=True, text=True)
+    assert out.returncode == 0 and out.stdout.startswith("abi "), out.stdout + out.stderr

@@ -101,3 +101,15 @@ def test_baseline_configs_from_the_cli(cli, oracle):
             assert (j["m"], j["nnz"], j["d"]) == (a.m, a.nnz, spec["d"])
             assert j["y_checksum"] == want
     assert run(cli, "--config", "c9").returncode == 1
+
+
+def test_plain_c_caller_of_the_abi(tmp_path):
+    """examples/spmx_minimal.c: the reference's worked example (test_matrix_core.cpp:181-189) from a
+    C99 program with malloc'ed arrays, every strategy, both modes, and the reference's shape error."""
+    import subprocess
+    import sys
+    sys.path.insert(0, os.path.dirname(os.path.abspath(__file__)))
+    from test_abi_cpu import _build_c_example
+    out = subprocess.run([_build_c_example(tmp_path)], capture_output=True, text=True, timeout=120)
+    assert out.returncode == 0, out.stdout + out.stderr
+    assert "worked example ok" in out.stdout
