@@ -99,3 +99,29 @@ def test_invalid_matrix_from_pageable_arrays_is_einval(case):
     y1, _ = ctx.spmm_host(a.m, a.n, rp, col, vals, xn, strategy="merge", nnz=a.nnz)
     assert np.array_equal(y0.view(np.uint32), y1.view(np.uint32)) and np.isfinite(y0).all()
     ctx.close()
+
+
+@pytest.mark.parametrize("nbytes", [(1 << 20) - 4, 1 << 20, (4 << 20) - 4, 4 << 20, (4 << 20) + 4, (8 << 20) + 12,
+                                    (33 << 20) + 20, (64 << 20) - 8])
+def test_staged_copies_round_trip(nbytes):
+    """spmx_h2d / spmx_d2h with pageable arrays whose sizes sit on and around the stager's 1 MB
+    threshold and 4 MB piece boundaries, at a misaligned host address: up, down, same bytes, and
+    nothing written outside the destination."""
+    import ctypes as C
+    from paper_2312_05639_b200.binding import Context
+    ctx = Context(0)
+    rng = np.random.default_rng(nbytes)
+    src_buf = rng.integers(0, 256, nbytes + 64, dtype=np.uint8)
+    dst_buf = np.full(nbytes + 128, 0xA5, np.uint8)
+    src = src_buf[4:4 + nbytes]              # 4-byte offsets into the allocations
+    dst = dst_buf[36:36 + nbytes]
+    dev = torch.empty(nbytes, dtype=torch.uint8, device="cuda")
+    L = ctx.L
+    L.check(L.lib.spmx_h2d(ctx.h, C.c_void_p(dev.data_ptr()), C.c_void_p(src.ctypes.data), C.c_size_t(nbytes)))
+    ctx.synchronize()
+    assert np.array_equal(dev.cpu().numpy(), src)
+    L.check(L.lib.spmx_d2h(ctx.h, C.c_void_p(dst.ctypes.data), C.c_void_p(dev.data_ptr()), C.c_size_t(nbytes)))
+    ctx.synchronize()
+    assert np.array_equal(dst, src)
+    assert (dst_buf[:36] == 0xA5).all() and (dst_buf[36 + nbytes:] == 0xA5).all()
+    ctx.close()
