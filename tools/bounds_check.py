@@ -20,7 +20,8 @@ ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 sys.path.insert(0, ROOT)
 LIB = os.path.join(ROOT, "build", "libspmx_bounds.so")
 SUITES = ["tests/test_spmm_gpu.py", "tests/test_windows_gpu.py", "tests/test_edge_gpu.py", "tests/test_fuzz_gpu.py",
-          "tests/test_mg_gpu.py", "tests/test_partition_gpu.py"]
+          "tests/test_mg_gpu.py", "tests/test_partition_gpu.py", "tests/test_huge_nnz_gpu.py",
+          "tests/test_pageable_host_gpu.py", "tests/test_graph_capture_gpu.py"]
 
 
 def build():
